@@ -1,0 +1,483 @@
+#!/usr/bin/env python
+"""bench.py — lattice updates per second of the two-step march on B200.
+
+Default workload (N=1): BASELINE config 4 — P9 nine-point scheme, 32768^2 f64 grid,
+Dirichlet zero ring of width 1, λ=0.6, seeded 64-Gaussian u0 and v0=0 (the
+largest single-GPU configuration the metric's 1/2/4/8-GPU numbers are quoted on;
+see DESIGN.md §Measurement).  One "step" = one two-step update of the whole grid.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5|C3f32]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+For N>1 run under torchrun: one process per GPU, row slabs, halo rows over NCCL
+(``scaling: strong`` — the grid is fixed).  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-point updates/sec (GLUP/s) and fraction of HBM roofline, 1/2/4/8 B200"
+
+CONFIGS = {
+    "C1": dict(scheme="P5", n=511, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.5,
+               steps=200, ic="gauss-centre",
+               desc="C1: P5 5-point, 512^2 f64, Dirichlet ring 1, lambda=0.5, 200 steps"),
+    "C2": dict(scheme="P9", n=4096, bc="periodic", ring=0, dtype="f64", arith="ref", lam=0.6,
+               steps=1000, ic="standing",
+               desc="C2: P9 9-point, 4096^2 f64 periodic, lambda=0.6, standing wave m=4 n=6, 1000 steps"),
+    "C3": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f64", arith="ref", lam=0.4,
+               steps=500, ic=(32, 0.01, 0.05, False),
+               desc="C3: P13 13-point, 16384^2 f64, Dirichlet ring 2, lambda=0.4, 500 steps"),
+    "C3f32": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f32", arith="native",
+                  lam=0.4, steps=500, ic=(32, 0.01, 0.05, False),
+                  desc="C3: P13 13-point, 16384^2 f32, Dirichlet ring 2, lambda=0.4, 500 steps"),
+    "C4": dict(scheme="P9", n=32767, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.6,
+               steps=200, ic=(64, 0.01, 0.05, True),
+               desc="C4: P9 9-point, 32768^2 f64, Dirichlet ring 1, lambda=0.6, 200 steps"),
+    "C5": dict(scheme="P13", n=65535, bc="dirichlet", ring=2, dtype="f32", arith="native",
+               lam=0.4, steps=100, ic=(128, 0.002, 0.01, False),
+               desc="C5: P13 13-point, 65536^2 f32, Dirichlet ring 2, lambda=0.4, 100 steps"),
+}
+
+REASONS = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(cfg_name):
+    path = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(r)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gpu_id(local: int) -> str:
+    """nvidia-smi -i accepts the GPU UUID, which survives CUDA_VISIBLE_DEVICES remapping."""
+    try:
+        import torch
+
+        uuid = str(torch.cuda.get_device_properties(local).uuid)
+        return uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"
+    except Exception:
+        return str(local)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def cpu_sample(cfg, seconds: float, threads: int = 0, rows_hint: int | None = None):
+    """Time the oracle (the reference's arithmetic restated in C, OpenMP over rows) on a
+    full-width row slab of the config's grid.  Returns (LUP/s, rows, steps, secs)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_1904_04048_b200.scheme import evaluate_table, named_scheme
+
+    spec = named_scheme(cfg["scheme"])
+    pairs = evaluate_table(spec.two_step, cfg["lam"])
+    width = cfg["n"] + 1
+    ring = cfg["ring"] if cfg["bc"] == "dirichlet" else 0
+    npdt = np.float64 if cfg["dtype"] == "f64" else np.float32
+    arith = cfg["arith"]
+
+    def run(rows, steps):
+        rng = np.random.default_rng(0)
+        a = rng.standard_normal((rows + 2 * max(ring, 1), width)).astype(npdt)
+        b = rng.standard_normal(a.shape).astype(npdt)
+        bc = cfg["bc"]
+        t0 = time.perf_counter()
+        O.march(a, b, pairs, steps, bc, max(ring, 1) if bc == "dirichlet" else 0, arith, threads)
+        dt = time.perf_counter() - t0
+        inner = rows * (width - 2 * ring)
+        return inner * steps / dt, dt
+
+    rows = rows_hint or 32
+    rate, dt = run(rows, 1)
+    # size the slab so one step takes ~seconds/4, then run 4 steps
+    per_row = dt / rows
+    rows = int(max(16, min(width, (seconds / 4.0) / max(per_row, 1e-9))))
+    rate, dt = run(rows, 4)
+    return rate, rows, 4, dt
+
+
+def reference_arm(args, cfg, cfg_name):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    threads = O.max_threads()
+    rate0, rows, _, _ = cpu_sample(cfg, 2.0)
+    # per step: a full-width slab sized for ~0.25 s so K + W steps stay within minutes
+    import numpy as np
+
+    from paper_1904_04048_b200.scheme import evaluate_table, named_scheme
+
+    spec = named_scheme(cfg["scheme"])
+    pairs = evaluate_table(spec.two_step, cfg["lam"])
+    width = cfg["n"] + 1
+    ring = max(cfg["ring"], 1) if cfg["bc"] == "dirichlet" else 0
+    lup_row = width - 2 * (cfg["ring"] if cfg["bc"] == "dirichlet" else 0)
+    srows = int(max(8, min(width, 0.25 * rate0 / lup_row)))
+    npdt = np.float64 if cfg["dtype"] == "f64" else np.float32
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((srows + 2 * max(ring, 1), width)).astype(npdt)
+    b = rng.standard_normal(a.shape).astype(npdt)
+    for _ in range(args.warmup):
+        b = O.two_step(a, b, pairs, cfg["bc"], ring, cfg["arith"])
+        a, b = b, a
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        b = O.two_step(a, b, pairs, cfg["bc"], ring, cfg["arith"])
+        a, b = b, a
+    dt = time.perf_counter() - t0
+    lup = srows * lup_row * args.steps
+    value = lup / dt / 1e9
+    sample = (f"{srows} full-width rows x {width} cols per step (of {cfg['n'] + 1} rows), "
+              f"{args.steps} steps")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+        "config": {"workload": cfg["desc"], "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": threads, "kind": "port",
+                         "sample": sample + "; oracle/ps_oracle.c (reference arithmetic, "
+                                   "OpenMP over rows)"},
+        "e2e": {"value": value, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def make_sim(cfg):
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation(cfg["scheme"], cfg["n"], cfg["lam"], bc=cfg["bc"],
+                     ring=cfg["ring"] if cfg["bc"] == "dirichlet" else None,
+                     dtype=cfg["dtype"], arith=cfg["arith"])
+    ic = cfg["ic"]
+    if ic == "standing":
+        sim.standing_wave_initial(4, 6)
+    elif ic == "gauss-centre":
+        import numpy as np
+
+        n = cfg["n"]
+        x = np.arange(n + 1) / n
+        x1, x2 = np.meshgrid(x, x, indexing="ij")
+        sim.load_initial(np.exp(-((x1 - 0.5) ** 2 + (x2 - 0.5) ** 2) / (2 * 0.05**2)), None)
+    else:
+        K, wmin, wmax, vzero = ic
+        sim.gaussian_initial(K, wmin, wmax, seed=0, v_zero=vzero)
+    return sim
+
+
+def gpu_arm_single(args, cfg, cfg_name):
+    import numpy as np
+    import torch
+
+    from paper_1904_04048_b200 import _native as nat
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    sim = make_sim(cfg)
+    sim.first_step()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        sim.march(1)
+    torch.cuda.synchronize()
+
+    lup_step = sim.updated_nodes
+    bytes_launch = 3 * sim.itemsize * lup_step
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = nat.launch_count()
+    with ClockSampler(gpu_id(0)) as clk:
+        torch.cuda.synchronize()
+        t_begin.record(stream)
+        for k in range(K):
+            starts[k].record(stream)
+            sim.march(1)
+            ends[k].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = nat.launch_count() - launches0
+    total_ms = t_begin.elapsed_time(t_end)
+    per_launch = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    avg_launch_ms = sum(per_launch) / len(per_launch)
+    value = lup_step * K / (total_ms * 1e-3) / 1e9
+    peak, peak_src = load_peak()
+    achieved = bytes_launch / (avg_launch_ms * 1e-3) / 1e9
+    traffic = load_traffic(cfg_name)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GLUP/s", "n_gpus": 1, "steps": K,
+        "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
+        "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
+                   "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
+                   "parallelism": "single GPU",
+                   "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
+                         "3 levels streamed per step" if sim.level_bytes > 126e6 else
+                         "grid fits in L2 (latency-bound correctness config)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_launch,
+                     "kernel_ms_per_launch": avg_launch_ms,
+                     "lup_per_launch": lup_step, "bytes_per_lup": 3 * sim.itemsize},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    del per_launch
+    if not args.no_e2e:
+        line["e2e"] = e2e_single(args, cfg, sim)
+    if not args.no_cpu:
+        from oracle import oracle as O
+
+        rate, rows, steps, secs = cpu_sample(cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": rate / 1e9, "unit": "GLUP/s", "cores": O.max_threads(), "kind": "port",
+            "sample": f"{rows} full-width rows x {cfg['n'] + 1} cols, {steps} two-step updates "
+                      f"({secs:.1f} s) through oracle/ps_oracle.c (reference arithmetic, OpenMP)"}
+    print(json.dumps(line), flush=True)
+
+
+def e2e_single(args, cfg, sim):
+    """Same metric through the public device API with host buffers: pinned u0 (v0) ->
+    device, first step + (K-1) two-steps, newest level -> pinned host, all timed."""
+    import torch
+
+    from paper_1904_04048_b200 import _native as nat
+
+    n1 = cfg["n"] + 1
+    u0_host, v0_host = sim.initial_fields()
+    npdt = u0_host.dtype
+    tdt = torch.float64 if npdt.itemsize == 8 else torch.float32
+    pin_u = torch.from_numpy(u0_host).pin_memory()
+    vzero = isinstance(cfg["ic"], tuple) and cfg["ic"][3]
+    pin_v = None if vzero else torch.from_numpy(v0_host).pin_memory()
+    del u0_host, v0_host
+    out = torch.empty((n1, n1), dtype=tdt).pin_memory()
+    st = nat.current_stream()
+    lib = nat.load_library()
+    import ctypes
+
+    g = sim.grid
+    K = args.steps
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    nat.check(lib.ps_copy_in(ctypes.byref(g), sim.levels[1].ptr, ctypes.c_void_p(pin_u.data_ptr()),
+                             n1, n1, n1, nat.H2D, st), "ps_copy_in")
+    if pin_v is None:
+        sim.levels[0].buf.zero_()
+    else:
+        nat.check(lib.ps_copy_in(ctypes.byref(g), sim.levels[0].ptr,
+                                 ctypes.c_void_p(pin_v.data_ptr()), n1, n1, n1, nat.H2D, st),
+                  "ps_copy_in")
+    if cfg["bc"] == "periodic":
+        sim.levels[1].fill_ghosts()
+        sim.levels[0].fill_ghosts()
+    sim.first_step()
+    sim.march(K - 1)
+    nat.check(lib.ps_copy_out(ctypes.byref(g), sim.levels[sim.newest].ptr,
+                              ctypes.c_void_p(out.data_ptr()), n1, n1, n1, nat.D2H, st),
+              "ps_copy_out")
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    h2d = pin_u.numel() * pin_u.element_size() * (1 if pin_v is None else 2)
+    d2h = out.numel() * out.element_size()
+    return {"value": sim.updated_nodes * K / (ms * 1e-3) / 1e9, "unit": "GLUP/s",
+            "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+            "ms_total": ms,
+            "what": "ps_copy_in(u0[,v0]) from pinned host + ps_first_step + (K-1) ps_two_step + "
+                    "ps_copy_out(u^K) to pinned host, one CUDA-event-timed region"}
+
+
+def gpu_arm_dist(args, cfg, cfg_name):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1904_04048_b200 import _native as nat
+    from paper_1904_04048_b200.device import gaussian_params
+    from paper_1904_04048_b200.slab import DistributedSlabs
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if cfg["bc"] != "dirichlet" or not isinstance(cfg["ic"], tuple):
+        raise SystemExit("multi-GPU bench supports the Dirichlet Gaussian configs (C3-C5)")
+    slab = DistributedSlabs(cfg["scheme"], cfg["n"], cfg["lam"], ring=cfg["ring"],
+                            dtype=cfg["dtype"], arith=cfg["arith"])
+    K0, wmin, wmax, vzero = cfg["ic"]
+    rng = np.random.default_rng(0)
+    pu = gaussian_params(rng, K0, wmin, wmax)
+    nat.gaussian_sum(slab.grid, slab.levels[1], pu[0], pu[1], pu[2], cfg["n"])
+    if vzero:
+        slab.levels[0].buf.zero_()
+    else:
+        pv = gaussian_params(rng, K0, wmin, wmax)
+        nat.gaussian_sum(slab.grid, slab.levels[0], pv[0], pv[1], pv[2], cfg["n"])
+    slab.exchange(1)
+    slab.exchange(0)
+    slab.first_step()
+    for _ in range(args.warmup):
+        slab.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    K = args.steps
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = nat.launch_count()
+    with ClockSampler(gpu_id(local)) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0.record()
+        for _ in range(K):
+            slab.step()
+        t1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    launches = nat.launch_count() - launches0
+    ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    inner = cfg["n"] + 1 - 2 * cfg["ring"]
+    lup_step = inner * inner
+    value = lup_step * K / (total_ms * 1e-3) / 1e9
+    itemsize = 8 if cfg["dtype"] == "f64" else 4
+    peak, peak_src = load_peak()
+    achieved = 3 * itemsize * lup_step / world / (total_ms / K * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
+            "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
+            "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
+                       "lambda": cfg["lam"], "arith": cfg["arith"],
+                       "parallelism": f"row slabs x{world}, {slab.R}-row halo over NCCL send/recv "
+                                      "overlapped with the interior update",
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": load_traffic(cfg_name),
+                         "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)"},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+            "e2e": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = cfg["steps"]
+    args.warmup = max(args.warmup, 0)
+    world, rank, _ = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, cfg, args.config)
+        return
+    if world > 1:
+        gpu_arm_dist(args, cfg, args.config)
+    else:
+        gpu_arm_single(args, cfg, args.config)
+
+
+if __name__ == "__main__":
+    main()

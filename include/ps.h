@@ -1,0 +1,166 @@
+/*
+ * ps.h — C-ABI of libps.so, the B200 (sm_100a) engine behind the poisson_stencils
+ * drop-in.  Plain pointers and sizes only; no torch or numpy types cross this line.
+ *
+ * The reference (poisson-stencils 0.1.0, pure Python/numpy) has no FFI.  Each entry
+ * point below replaces one reference function; the citation names the file:line of the
+ * function it stands in for (paths relative to the reference's pkg/src/poisson_stencils/).
+ * INTEGRATION.md shows the ctypes binding a maintainer adds on the reference side.
+ *
+ * Conventions
+ *   - Field pointers ("levels") are DEVICE pointers to an allocation laid out by
+ *     ps_layout_init(): logical element (i, j) lives at  level[grid->origin + i*pitch + j].
+ *     Around the logical rows x cols block the allocation holds `ghost` padding rows above
+ *     and below and >= 16 bytes of padding columns on each side.  Periodic grids keep
+ *     their wrap-around images (rows/cols -ghost..-1 and n..n+ghost-1) in that padding;
+ *     every kernel that writes a periodic level also refreshes its images.
+ *   - Logical extent: Dirichlet grids hold all (n+1) x (n+1) nodes (ring included);
+ *     periodic grids hold the n x n independent nodes; the reference's alias row/col n
+ *     is the first image row/col.
+ *   - Calls are asynchronous on the given stream (NULL = legacy default stream), never
+ *     allocate, keep no global mutable state, and are safe from concurrent threads.
+ *   - Return 0 (PS_OK) or a distinct ps_status; ps_strerror() names it.
+ */
+#ifndef PS_H_
+#define PS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ps_status {
+  PS_OK = 0,
+  PS_ERR_ARG = 1,        /* bad argument (null pointer, bad enum, negative size)          */
+  PS_ERR_SHAPE = 2,      /* grid too small for the stencil / layout mismatch              */
+  PS_ERR_TABLE = 3,      /* coefficient table empty, too long or offsets beyond the ghost */
+  PS_ERR_RADIUS = 4,     /* Dirichlet ring narrower than the stencil radius (cli.py:24)   */
+  PS_ERR_CUDA = 5,       /* a CUDA runtime call failed                                    */
+  PS_ERR_ALIGN = 6       /* level pointer not 16-byte aligned                             */
+} ps_status;
+
+typedef enum ps_bc { PS_BC_DIRICHLET = 0, PS_BC_PERIODIC = 1 } ps_bc;
+typedef enum ps_dtype { PS_F64 = 0, PS_F32 = 1 } ps_dtype;
+
+/* Arithmetic contract.
+ *   PS_ARITH_REF    — the reference's own operation sequence, bit for bit (simulator.py:147-191):
+ *                     f64: acc = +0.0; acc = fl(acc + fl(c*u)) in table order, no FMA;
+ *                     f32: products in f32, accumulation in f64, cast to f32, f32 subtract.
+ *   PS_ARITH_NATIVE — f32 only: the same ordered, FMA-free sequence carried out entirely in
+ *                     f32 (no f64 accumulator).  Compared against the f64 oracle within a
+ *                     stated tolerance.  For f64 it is identical to PS_ARITH_REF. */
+typedef enum ps_arith { PS_ARITH_REF = 0, PS_ARITH_NATIVE = 1 } ps_arith;
+
+#define PS_MAX_TAPS 32
+#define PS_MAX_GHOST 8
+
+/* One coefficient table evaluated at the Courant number, in the reference's dict order
+ * (scheme.py:26-51 tables, evaluated by simulator.py:131-132 -> quadrature.py:107-108).
+ * Tap s reads u[i + q1[s], j + q2[s]] (q1 along axis 0 = x1, q2 along axis 1 = x2). */
+typedef struct ps_table {
+  int32_t ntaps;
+  int32_t q1[PS_MAX_TAPS];
+  int32_t q2[PS_MAX_TAPS];
+  double c[PS_MAX_TAPS];
+} ps_table;
+
+/* Geometry and numerics of one family of levels; filled by ps_layout_init(). */
+typedef struct ps_grid {
+  int64_t rows;    /* logical rows  (Dirichlet n+1, periodic n)             */
+  int64_t cols;    /* logical cols                                          */
+  int64_t pitch;   /* elements between consecutive rows (multiple of 128 B) */
+  int64_t origin;  /* element offset of logical (0,0) from the allocation   */
+  int64_t ghost;   /* padding rows above/below the logical block            */
+  int64_t row0;    /* global index of logical row 0 (row slabs; else 0)     */
+  int64_t grows;   /* global logical rows (row slabs; else == rows)         */
+  int32_t ring;    /* Dirichlet: width of the pinned zero ring; periodic: 0 */
+  int32_t bc;      /* ps_bc    */
+  int32_t dtype;   /* ps_dtype */
+  int32_t arith;   /* ps_arith */
+} ps_grid;
+
+/* Fill *g for a rows x cols grid.  `ghost` = largest stencil radius the levels must
+ * serve (>= 1; rounded up to 2).  `ring` = Dirichlet ring width (ignored for periodic).
+ * Replaces the implicit layout of numpy arrays allocated per step (simulator.py:150). */
+ps_status ps_layout_init(ps_grid* g, int64_t rows, int64_t cols, int32_t ghost, int32_t ring,
+                         int32_t bc, int32_t dtype, int32_t arith);
+/* Row slab of a global grid for the multi-GPU decomposition: the
+ * level holds global rows [row0, row0 + rows) as logical rows 0..rows-1; its `ghost`
+ * padding rows receive the neighbours' halo rows (global rows row0-ghost.. and
+ * row0+rows..).  Dirichlet ring masking uses global indices against `grows`.
+ * Periodic slabs wrap columns locally and rows through the halo exchange. */
+ps_status ps_slab_layout_init(ps_grid* g, int64_t grows, int64_t cols, int64_t row0,
+                              int64_t rows, int32_t ghost, int32_t ring, int32_t bc,
+                              int32_t dtype, int32_t arith);
+
+/* Bytes one level of *g occupies. */
+size_t ps_level_bytes(const ps_grid* g);
+
+/* Convenience allocation for callers without their own allocator (ctypes users).
+ * The level is zero-filled.  Returns NULL on failure. */
+void* ps_level_alloc(const ps_grid* g);
+void ps_level_free(void* level);
+
+/* Copy a dense host/device rows_h x cols_h block (row stride host_pitch elements) into /
+ * out of the logical block of a level, starting at logical (0,0).  rows_h/cols_h may
+ * exceed rows/cols by up to `ghost` for periodic grids (the reference's alias row/col).
+ * `kind`: cudaMemcpyKind value (1 = H2D, 2 = D2H, 3 = D2D, 4 = default). */
+ps_status ps_copy_in(const ps_grid* g, void* level, const void* src, int64_t rows_h,
+                     int64_t cols_h, int64_t src_pitch, int32_t kind, void* stream);
+ps_status ps_copy_out(const ps_grid* g, const void* level, void* dst, int64_t rows_h,
+                      int64_t cols_h, int64_t dst_pitch, int32_t kind, void* stream);
+
+/* Periodic: refresh every image position from the core (simulator.py:135-138,
+ * _alias_edges).  keep_alias != 0 leaves the reference's alias row n / col n
+ * (0 <= i,j <= n) untouched, so a caller-supplied u^{k-1} alias survives (simulator.py:184).
+ * Dirichlet: no-op. */
+ps_status ps_fill_ghosts(const ps_grid* g, void* level, int32_t keep_alias, void* stream);
+
+/* First time step  u1 = A_u(u0) + fl(tau * A_v(v0))  (simulator.py:166-180, run() 269-270). */
+ps_status ps_first_step(const ps_grid* g, const void* u0, const void* v0, void* u1,
+                        const ps_table* tu, const ps_table* tv, double tau, void* stream);
+
+/* Two-step update  u^{k+1} = A(u^k) - u^{k-1}, ring re-pinned / images refreshed
+ * (simulator.py:183-205).  ukp1 must not alias uk; it MAY alias ukm1 (each point of
+ * u^{k-1} is read only by the thread that overwrites it). */
+ps_status ps_two_step(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                      const ps_table* t, void* stream);
+
+/* ps_two_step restricted to logical rows [row_lo, row_hi): lets a slab update its
+ * boundary rows first, hand them to the halo exchange, and update the interior
+ * concurrently. */
+ps_status ps_two_step_rows(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                           const ps_table* t, int64_t row_lo, int64_t row_hi, void* stream);
+
+/* nsteps two-step updates rotating three levels in place (the loop of run(),
+ * simulator.py:271-274).  On entry lvl[*newest] = u^k and lvl[(*newest+2)%3] = u^{k-1};
+ * on return *newest names the level holding the last update. */
+ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
+                   int32_t* newest, void* stream);
+
+/* Sum of K isotropic Gaussians sampled at x1 = i/n, x2 = j/n (the reference's node
+ * coordinates np.arange(n+1)/n, simulator.py:254-255) in f64, k order:
+ *   u = sum_k amp[k] * exp(-((x1-cx[k])^2 + (x2-cy[k])^2) / (2*(width[k]^2)))
+ * written in the level's dtype (BASELINE configs 3-5 initial data; the reference's
+ * _sample, simulator.py:141-144, evaluates user callables on the same nodes).
+ * Dirichlet: the whole (n+1)^2 block incl. ring; periodic: the core, then its images.
+ * The parameter arrays are HOST pointers (copied into the launch, K <= 512). */
+ps_status ps_gaussian_sum(const ps_grid* g, void* level, int32_t K, const double* cx,
+                          const double* cy, const double* width, const double* amp,
+                          int64_t n, void* stream);
+
+/* Kernel launches issued by this library since load (for launch accounting). */
+int64_t ps_launch_count(void);
+
+/* Static description of a ps_status. */
+const char* ps_strerror(int32_t status);
+
+/* Library version string ("paper_1904_04048_b200 <semver> sm_100a"). */
+const char* ps_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PS_H_ */

@@ -1,0 +1,236 @@
+"""ctypes binding of libps.so (the C-ABI in include/ps.h) plus device-level plumbing.
+
+Device memory and streams come from PyTorch (plumbing only); every byte of stencil
+arithmetic runs in libps.so's sm_100a kernels.  There is no CPU fallback: if the
+library is missing or no CUDA device is visible, every entry point raises
+:class:`NativeUnavailableError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libps.so")
+
+PS_MAX_TAPS = 32
+BC = {"dirichlet": 0, "periodic": 1}
+DTYPE = {"f64": 0, "f32": 1}
+ARITH = {"ref": 0, "native": 1}
+NP_DTYPE = {"f64": np.float64, "f32": np.float32}
+H2D, D2H, D2D = 1, 2, 3
+
+
+class NativeUnavailableError(RuntimeError):
+    """libps.so is not built or no CUDA device is available; there is no fallback."""
+
+
+class PsStatusError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: {strerror(status)} (ps_status {status})")
+        self.status = status
+
+
+class PsGrid(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("pitch", ctypes.c_int64),
+                ("origin", ctypes.c_int64), ("ghost", ctypes.c_int64), ("row0", ctypes.c_int64),
+                ("grows", ctypes.c_int64), ("ring", ctypes.c_int32),
+                ("bc", ctypes.c_int32), ("dtype", ctypes.c_int32), ("arith", ctypes.c_int32)]
+
+
+class PsTable(ctypes.Structure):
+    _fields_ = [("ntaps", ctypes.c_int32), ("q1", ctypes.c_int32 * PS_MAX_TAPS),
+                ("q2", ctypes.c_int32 * PS_MAX_TAPS), ("c", ctypes.c_double * PS_MAX_TAPS)]
+
+
+EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
+           "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
+           "ps_march",
+           "ps_gaussian_sum", "ps_launch_count", "ps_strerror", "ps_version")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libps.so and declare its signatures (no GPU needed to load)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailableError(
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(path)
+        i64, i32, vp, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double
+        G, T = ctypes.POINTER(PsGrid), ctypes.POINTER(PsTable)
+        sig = {
+            "ps_layout_init": (i32, [G, i64, i64, i32, i32, i32, i32, i32]),
+            "ps_slab_layout_init": (i32, [G, i64, i64, i64, i64, i32, i32, i32, i32, i32]),
+            "ps_level_bytes": (ctypes.c_size_t, [G]),
+            "ps_level_alloc": (vp, [G]),
+            "ps_level_free": (None, [vp]),
+            "ps_copy_in": (i32, [G, vp, vp, i64, i64, i64, i32, vp]),
+            "ps_copy_out": (i32, [G, vp, vp, i64, i64, i64, i32, vp]),
+            "ps_fill_ghosts": (i32, [G, vp, i32, vp]),
+            "ps_first_step": (i32, [G, vp, vp, vp, T, T, dbl, vp]),
+            "ps_two_step": (i32, [G, vp, vp, vp, T, vp]),
+            "ps_two_step_rows": (i32, [G, vp, vp, vp, T, i64, i64, vp]),
+            "ps_march": (i32, [G, ctypes.POINTER(vp), i64, T, ctypes.POINTER(i32), vp]),
+            "ps_gaussian_sum": (i32, [G, vp, i32, vp, vp, vp, vp, i64, vp]),
+            "ps_launch_count": (i64, []),
+            "ps_strerror": (ctypes.c_char_p, [i32]),
+            "ps_version": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return L
+
+
+def strerror(status: int) -> str:
+    try:
+        return load_library().ps_strerror(status).decode()
+    except NativeUnavailableError:
+        return f"status {status}"
+
+
+def check(status: int, what: str):
+    if status != 0:
+        raise PsStatusError(status, what)
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError(
+            "no CUDA device visible: the poisson_stencils GPU path has no CPU fallback")
+    return torch
+
+
+def current_stream():
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def make_table(pairs) -> PsTable:
+    """Pack ``[((q1, q2), coeff), ...]`` (dict order) into a ``ps_table``."""
+    pairs = list(pairs)
+    if not 1 <= len(pairs) <= PS_MAX_TAPS:
+        raise ValueError(f"tables must hold 1..{PS_MAX_TAPS} taps, got {len(pairs)}")
+    t = PsTable()
+    t.ntaps = len(pairs)
+    for s, ((q1, q2), c) in enumerate(pairs):
+        t.q1[s], t.q2[s], t.c[s] = int(q1), int(q2), float(c)
+    return t
+
+
+def make_slab_grid(grows, cols, row0, rows, ghost, ring, bc, dtype, arith="ref") -> PsGrid:
+    g = PsGrid()
+    check(load_library().ps_slab_layout_init(ctypes.byref(g), int(grows), int(cols), int(row0),
+                                             int(rows), int(ghost), int(ring), BC[bc],
+                                             DTYPE[dtype], ARITH[arith]), "ps_slab_layout_init")
+    return g
+
+
+def make_grid(rows, cols, ghost, ring, bc, dtype, arith="ref") -> PsGrid:
+    g = PsGrid()
+    check(load_library().ps_layout_init(ctypes.byref(g), int(rows), int(cols), int(ghost),
+                                        int(ring), BC[bc], DTYPE[dtype], ARITH[arith]),
+          "ps_layout_init")
+    return g
+
+
+class Level:
+    """One device level laid out by ``ps_layout_init`` (torch owns the bytes)."""
+
+    def __init__(self, grid: PsGrid, device=None):
+        torch = _torch()
+        self.grid = grid
+        nbytes = load_library().ps_level_bytes(ctypes.byref(grid))
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device or "cuda")
+        self.ptr = ctypes.c_void_p(self.buf.data_ptr())
+
+    @property
+    def np_dtype(self):
+        return np.float64 if self.grid.dtype == 0 else np.float32
+
+    def view(self):
+        """torch view of the logical rows x cols block (strided, zero-copy)."""
+        torch = _torch()
+        tdt = torch.float64 if self.grid.dtype == 0 else torch.float32
+        flat = self.buf.view(tdt)
+        return flat.as_strided((self.grid.rows, self.grid.cols), (self.grid.pitch, 1),
+                               self.grid.origin)
+
+    def upload(self, host: np.ndarray, stream=None):
+        host = np.ascontiguousarray(host, dtype=self.np_dtype)
+        check(load_library().ps_copy_in(ctypes.byref(self.grid), self.ptr,
+                                        host.ctypes.data_as(ctypes.c_void_p), host.shape[0],
+                                        host.shape[1], host.shape[1], H2D,
+                                        stream or current_stream()), "ps_copy_in")
+        # pageable source: the copy has been staged before return; keep `host` alive anyway
+        self._keep = host
+
+    def download(self, rows=None, cols=None, stream=None) -> np.ndarray:
+        rows = self.grid.rows if rows is None else rows
+        cols = self.grid.cols if cols is None else cols
+        out = np.empty((rows, cols), dtype=self.np_dtype)
+        st = stream or current_stream()
+        check(load_library().ps_copy_out(ctypes.byref(self.grid), self.ptr,
+                                         out.ctypes.data_as(ctypes.c_void_p), rows, cols, cols,
+                                         D2H, st), "ps_copy_out")
+        _torch().cuda.current_stream().synchronize()
+        return out
+
+    def fill_ghosts(self, keep_alias=False, stream=None):
+        check(load_library().ps_fill_ghosts(ctypes.byref(self.grid), self.ptr, int(keep_alias),
+                                            stream or current_stream()), "ps_fill_ghosts")
+
+
+def first_step(grid, u0: Level, v0: Level, out: Level, tu: PsTable, tv: PsTable, tau, stream=None):
+    check(load_library().ps_first_step(ctypes.byref(grid), u0.ptr, v0.ptr, out.ptr,
+                                       ctypes.byref(tu), ctypes.byref(tv), float(tau),
+                                       stream or current_stream()), "ps_first_step")
+
+
+def two_step(grid, uk: Level, ukm1: Level, out: Level, t: PsTable, stream=None):
+    check(load_library().ps_two_step(ctypes.byref(grid), uk.ptr, ukm1.ptr, out.ptr,
+                                     ctypes.byref(t), stream or current_stream()), "ps_two_step")
+
+
+def two_step_rows(grid, uk: Level, ukm1: Level, out: Level, t: PsTable, lo: int, hi: int,
+                  stream=None):
+    check(load_library().ps_two_step_rows(ctypes.byref(grid), uk.ptr, ukm1.ptr, out.ptr,
+                                          ctypes.byref(t), int(lo), int(hi),
+                                          stream or current_stream()), "ps_two_step_rows")
+
+
+def march(grid, levels, nsteps: int, t: PsTable, newest: int, stream=None) -> int:
+    arr = (ctypes.c_void_p * 3)(*[lv.ptr.value for lv in levels])
+    nw = ctypes.c_int32(newest)
+    check(load_library().ps_march(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
+                                  ctypes.byref(nw), stream or current_stream()), "ps_march")
+    return nw.value
+
+
+def gaussian_sum(grid, level: Level, centres, widths, amps, n: int, stream=None):
+    cx = np.ascontiguousarray([c[0] for c in centres], dtype=np.float64)
+    cy = np.ascontiguousarray([c[1] for c in centres], dtype=np.float64)
+    w = np.ascontiguousarray(widths, dtype=np.float64)
+    a = np.ascontiguousarray(amps, dtype=np.float64)
+    p = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    check(load_library().ps_gaussian_sum(ctypes.byref(grid), level.ptr, len(a), p(cx), p(cy),
+                                         p(w), p(a), int(n), stream or current_stream()),
+          "ps_gaussian_sum")
+
+
+def launch_count() -> int:
+    return int(load_library().ps_launch_count())

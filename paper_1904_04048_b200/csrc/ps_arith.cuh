@@ -1,0 +1,71 @@
+// ps_arith.cuh — per-point arithmetic contracts (see ps_arith in include/ps.h).
+//
+// The reference accumulates each stencil as  acc = zeros(); acc += coeff * shifted
+// (simulator.py:152-160): a +0.0 start, one rounded product and one rounded add per
+// tap, in table order, never fused.  Every operation below is an explicit _rn
+// intrinsic so nvcc cannot contract a multiply-add into an FMA.
+#pragma once
+
+namespace ps {
+
+enum { ARITH_REF = 0, ARITH_NATIVE = 1 };
+
+template <typename T, int A>
+struct Arith;
+
+// f64: the reference's float64 path (both contracts coincide).
+template <int A>
+struct Arith<double, A> {
+  using acc_t = double;
+  using coef_t = double;
+  __device__ __forceinline__ static acc_t zero() { return 0.0; }
+  __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, double u) {
+    return __dadd_rn(acc, __dmul_rn(c, u));
+  }
+  // u^{k+1} = acc - u^{k-1}            (simulator.py:184)
+  __device__ __forceinline__ static double two(acc_t acc, double ukm1) {
+    return __dsub_rn(acc, ukm1);
+  }
+  // u^1 = acc_u + tau * acc_v           (simulator.py:178-179)
+  __device__ __forceinline__ static double first(acc_t au, acc_t av, double tau) {
+    return __dadd_rn(au, __dmul_rn(tau, av));
+  }
+};
+
+// f32, reference contract: numpy multiplies a float32 field by a Python float in
+// float32, adds the product into the float64 accumulator, stores the accumulator
+// back into a float32 array and subtracts in float32 (simulator.py:150-154, 184).
+template <>
+struct Arith<float, ARITH_REF> {
+  using acc_t = double;
+  using coef_t = float;
+  __device__ __forceinline__ static acc_t zero() { return 0.0; }
+  __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, float u) {
+    return __dadd_rn(acc, static_cast<double>(__fmul_rn(c, u)));
+  }
+  __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
+    return __fsub_rn(__double2float_rn(acc), ukm1);
+  }
+  __device__ __forceinline__ static float first(acc_t au, acc_t av, float tau) {
+    return __fadd_rn(__double2float_rn(au), __fmul_rn(tau, __double2float_rn(av)));
+  }
+};
+
+// f32, native contract: the same ordered, unfused sequence entirely in float32.
+template <>
+struct Arith<float, ARITH_NATIVE> {
+  using acc_t = float;
+  using coef_t = float;
+  __device__ __forceinline__ static acc_t zero() { return 0.0f; }
+  __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, float u) {
+    return __fadd_rn(acc, __fmul_rn(c, u));
+  }
+  __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
+    return __fsub_rn(acc, ukm1);
+  }
+  __device__ __forceinline__ static float first(acc_t au, acc_t av, float tau) {
+    return __fadd_rn(au, __fmul_rn(tau, av));
+  }
+};
+
+}  // namespace ps

@@ -1,0 +1,133 @@
+"""Device-resident simulation: the march the BASELINE configs and bench.py run.
+
+The reference's ``run`` (simulator.py:231-290) allocates fresh numpy grids every step
+and always scores against an ``exact`` callable; it is fp64-only and supports only a
+ring of width 1.  :class:`Simulation` keeps three ps_grid levels resident in HBM,
+rotates them in place (``ps_march``), and adds what the BASELINE configs need:
+float32 fields, a Dirichlet zero ring as wide as the stencil radius,
+device-side seeded Gaussian-sum initial data and standing-wave data.
+Every update still goes through the same sm_100a kernels and arithmetic contract as
+the drop-in ``first_step`` / ``two_step``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from .scheme import SchemeSpec, evaluate_table, named_scheme
+
+
+def gaussian_params(rng: np.random.Generator, K: int, wmin: float, wmax: float):
+    """One field's Gaussian-sum parameters, drawn in the recipe's order
+    (SURVEY.md §8d D1): centres U[0.1,0.9]^2, widths U[wmin,wmax], amplitudes U[-1,1]."""
+    centres = rng.uniform(0.1, 0.9, size=(K, 2))
+    widths = rng.uniform(wmin, wmax, size=K)
+    amps = rng.uniform(-1.0, 1.0, size=K)
+    return centres, widths, amps
+
+
+class Simulation:
+    """One grid on one GPU: ``n`` intervals per axis, three resident levels.
+
+    Dirichlet grids hold (n+1)^2 nodes with a pinned zero ring of width ``ring``
+    (default: the scheme radius); periodic grids hold n^2 independent nodes."""
+
+    def __init__(self, scheme, n: int, lam: float, bc: str = "dirichlet", ring: int | None = None,
+                 dtype: str = "f64", arith: str = "ref", c: float = 1.0):
+        self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
+        if bc not in nat.BC:
+            raise ValueError(f"bc must be one of {tuple(nat.BC)}, got {bc!r}")
+        if dtype not in nat.DTYPE:
+            raise ValueError(f"dtype must be one of {tuple(nat.DTYPE)}, got {dtype!r}")
+        self.n, self.lam, self.bc, self.dtype, self.c = int(n), float(lam), bc, dtype, float(c)
+        self.tau = self.lam * (1.0 / self.n) / self.c
+        radius = self.spec.radius
+        self.ring = (radius if ring is None else int(ring)) if bc == "dirichlet" else 0
+        self.rows = self.n + 1 if bc == "dirichlet" else self.n
+        self.grid = nat.make_grid(self.rows, self.rows, max(2, radius), self.ring, bc, dtype, arith)
+        self.levels = [nat.Level(self.grid) for _ in range(3)]
+        self.t_first_u = nat.make_table(evaluate_table(self.spec.first_u, self.lam))
+        self.t_first_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
+        self.t_two = nat.make_table(evaluate_table(self.spec.two_step, self.lam))
+        self.newest = None  # index of the level holding the latest time level
+        self.step = 0       # time level held by levels[newest]
+
+    # ---- sizes --------------------------------------------------------------------
+    @property
+    def updated_nodes(self) -> int:
+        """Nodes one step updates (ring excluded) — the LUP count of one step."""
+        inner = self.rows - 2 * self.ring
+        return inner * inner
+
+    @property
+    def level_bytes(self) -> int:
+        return self.levels[0].buf.numel()
+
+    @property
+    def itemsize(self) -> int:
+        return 8 if self.dtype == "f64" else 4
+
+    # ---- initial data -----------------------------------------------------------------
+    def load_initial(self, u0: np.ndarray, v0: np.ndarray | None = None):
+        """Upload u0 (and v0; None = zero) as (n+1)^2 reference-layout arrays."""
+        self.levels[1].upload(u0)
+        if v0 is None:
+            self.levels[0].buf.zero_()
+        else:
+            self.levels[0].upload(v0)
+        if self.bc == "periodic":
+            self.levels[1].fill_ghosts()
+            self.levels[0].fill_ghosts()
+        self.newest, self.step = None, 0
+
+    def gaussian_initial(self, K: int, wmin: float, wmax: float, seed: int = 0,
+                         v_zero: bool = False):
+        """Seeded Gaussian-sum u0 (and v0) generated on the device (ps_gaussian_sum)."""
+        rng = np.random.default_rng(seed)
+        pu = gaussian_params(rng, K, wmin, wmax)
+        nat.gaussian_sum(self.grid, self.levels[1], pu[0], pu[1], pu[2], self.n)
+        pv = None
+        if v_zero:
+            self.levels[0].buf.zero_()
+        else:
+            pv = gaussian_params(rng, K, wmin, wmax)
+            nat.gaussian_sum(self.grid, self.levels[0], pv[0], pv[1], pv[2], self.n)
+        self.newest, self.step = None, 0
+        return pu, pv
+
+    def standing_wave_initial(self, m: int, k: int, omega: float | None = None):
+        """u0 = sin(2πm x1) sin(2πk x2), v0 = ω u0 (BASELINE config 2), sampled on the
+        host exactly like the reference's ``_sample`` (simulator.py:141-144)."""
+        coords = np.arange(self.n + 1) / self.n
+        x1, x2 = np.meshgrid(coords, coords, indexing="ij")
+        u0 = np.sin(2.0 * np.pi * m * x1) * np.sin(2.0 * np.pi * k * x2)
+        if omega is None:
+            omega = 2.0 * np.pi * self.c * np.sqrt(m * m + k * k)
+        self.load_initial(u0, omega * u0)
+        return omega
+
+    # ---- time stepping ----------------------------------------------------------------
+    def first_step(self, stream=None):
+        """u^1 from (u^0 = levels[1], v0 = levels[0]) into levels[2]."""
+        nat.first_step(self.grid, self.levels[1], self.levels[0], self.levels[2], self.t_first_u,
+                       self.t_first_v, self.tau, stream)
+        self.newest, self.step = 2, 1
+
+    def march(self, nsteps: int, stream=None):
+        """``nsteps`` two-step updates, rotating the three levels in place."""
+        if self.newest is None:
+            raise RuntimeError("call first_step() before march()")
+        self.newest = nat.march(self.grid, self.levels, nsteps, self.t_two, self.newest, stream)
+        self.step += int(nsteps)
+
+    # ---- read-back ----------------------------------------------------------------
+    def field(self, which: str = "newest") -> np.ndarray:
+        """Latest (or previous) level as the reference's (n+1)^2 array."""
+        idx = self.newest if which == "newest" else (self.newest + 2) % 3
+        return self.levels[idx].download(self.n + 1, self.n + 1)
+
+    def initial_fields(self):
+        """(u0, v0) as uploaded / generated (before the first step overwrites nothing)."""
+        return (self.levels[1].download(self.n + 1, self.n + 1),
+                self.levels[0].download(self.n + 1, self.n + 1))

@@ -1,0 +1,262 @@
+"""Row-slab domain decomposition.
+
+The two-step update reads only an r-neighbourhood, so the global grid splits into P
+contiguous row slabs with one halo exchange per step: each slab sends its first r rows
+of the newest level to the slab above and its last r rows to the slab below, where
+they land in the ghost padding rows (-r..-1 / rows..rows+r-1) the kernels already read.
+Per-point arithmetic is unchanged, so results are bitwise independent of P.
+
+* :func:`partition`, :class:`SlabPlan` — pure host logic (who owns which rows, which
+  rows go where), shared by every transport.
+* :class:`VirtualSlabs` — P slabs on ONE device, halo rows moved by device copies.
+  Tests the decomposition bit for bit without more GPUs.
+* :class:`DistributedSlabs` — one slab per rank (torchrun, one process per GPU),
+  halo rows exchanged with NCCL send/recv on a communication stream while the
+  interior rows update (boundary rows first, then exchange || interior).
+
+The reference has no parallel path; its spec permits row partitioning that is
+bitwise deterministic for a fixed partition count.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .scheme import SchemeSpec, evaluate_table, named_scheme
+
+
+def partition(grows: int, P: int) -> list[tuple[int, int]]:
+    """P contiguous (row0, rows) slabs covering [0, grows), sizes differing by <= 1."""
+    if P < 1 or P > grows:
+        raise ValueError(f"cannot split {grows} rows into {P} slabs")
+    base, extra = divmod(grows, P)
+    out, row0 = [], 0
+    for p in range(P):
+        rows = base + (1 if p < extra else 0)
+        out.append((row0, rows))
+        row0 += rows
+    return out
+
+
+@dataclass(frozen=True)
+class SlabPlan:
+    """Halo traffic of one slab: ``sends``/``recvs`` are (peer, first_local_row, nrows).
+
+    A send of local rows [a, a+r) to ``peer`` pairs with that peer's recv into its
+    ghost rows.  Dirichlet grids are a line (no wrap); periodic grids are a ring."""
+
+    rank: int
+    P: int
+    row0: int
+    rows: int
+    halo: int
+    up: int | None
+    down: int | None
+    sends: tuple[tuple[int, int, int], ...]
+    recvs: tuple[tuple[int, int, int], ...]
+
+    @staticmethod
+    def build(grows: int, P: int, rank: int, halo: int, periodic: bool) -> "SlabPlan":
+        parts = partition(grows, P)
+        row0, rows = parts[rank]
+        if rows < halo:
+            raise ValueError(f"slab of {rows} rows is thinner than the halo {halo}")
+        up = rank - 1 if rank > 0 else (P - 1 if periodic and P > 1 else None)
+        down = rank + 1 if rank < P - 1 else (0 if periodic and P > 1 else None)
+        sends, recvs = [], []
+        if up is not None:
+            sends.append((up, 0, halo))              # my top rows -> up's bottom ghosts
+            recvs.append((up, -halo, halo))          # up's bottom rows -> my top ghosts
+        if down is not None:
+            sends.append((down, rows - halo, halo))  # my bottom rows -> down's top ghosts
+            recvs.append((down, rows, halo))         # down's top rows -> my bottom ghosts
+        return SlabPlan(rank, P, row0, rows, halo, up, down, tuple(sends), tuple(recvs))
+
+
+def rows_view(level: nat.Level, first: int, count: int):
+    """Flat torch view of ``count`` full-pitch rows starting at logical row ``first``
+    (may be negative: ghost rows).  Rows are contiguous in the padded layout."""
+    g = level.grid
+    flat = level.buf.view(level.view().dtype)
+    start = (g.ghost + first) * g.pitch
+    return flat[start:start + count * g.pitch]
+
+
+class VirtualSlabs:
+    """P Dirichlet row slabs of one (n+1)^2 grid on one device (test vehicle)."""
+
+    def __init__(self, scheme, n: int, lam: float, P: int, ring: int | None = None,
+                 dtype: str = "f64", arith: str = "ref", c: float = 1.0):
+        self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
+        self.n, self.lam, self.P = int(n), float(lam), int(P)
+        self.tau = self.lam / self.n / c
+        R = self.spec.radius
+        self.ring = R if ring is None else int(ring)
+        grows = self.n + 1
+        self.plans = [SlabPlan.build(grows, P, p, R, periodic=False) for p in range(P)]
+        self.grids = [nat.make_slab_grid(grows, grows, pl.row0, pl.rows, max(2, R), self.ring,
+                                         "dirichlet", dtype, arith) for pl in self.plans]
+        self.levels = [[nat.Level(g) for _ in range(3)] for g in self.grids]
+        self.t_u = nat.make_table(evaluate_table(self.spec.first_u, self.lam))
+        self.t_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
+        self.t_two = nat.make_table(evaluate_table(self.spec.two_step, self.lam))
+        self.newest = None
+
+    def _exchange(self, idx: int):
+        for p, pl in enumerate(self.plans):
+            for peer, first, count in pl.sends:
+                dst_first = -count if peer > p else self.plans[peer].rows
+                rows_view(self.levels[peer][idx], dst_first, count).copy_(
+                    rows_view(self.levels[p][idx], first, count))
+
+    def load_initial(self, u0: np.ndarray, v0: np.ndarray):
+        for pl, lv in zip(self.plans, self.levels):
+            lv[1].upload(u0[pl.row0:pl.row0 + pl.rows])
+            lv[0].upload(v0[pl.row0:pl.row0 + pl.rows])
+        self._exchange(1)
+        self._exchange(0)
+
+    def first_step(self):
+        for g, lv in zip(self.grids, self.levels):
+            nat.first_step(g, lv[1], lv[0], lv[2], self.t_u, self.t_v, self.tau)
+        self._exchange(2)
+        self.newest = 2
+
+    def march(self, nsteps: int):
+        for _ in range(nsteps):
+            cur = self.newest
+            nxt, prev = (cur + 1) % 3, (cur + 2) % 3
+            for g, lv in zip(self.grids, self.levels):
+                nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
+            self._exchange(nxt)
+            self.newest = nxt
+
+    def field(self) -> np.ndarray:
+        return np.concatenate([lv[self.newest].download() for lv in self.levels], axis=0)
+
+
+class DistributedSlabs:
+    """This rank's Dirichlet row slab of an (n+1)^2 grid; halo exchange over
+    ``torch.distributed`` (NCCL on GPUs) overlapped with the interior update.
+
+    ``compute`` supplies the per-slab updates (``first_step(grid, u0, v0, out)`` and
+    ``two_step_rows(grid, uk, ukm1, out, lo, hi)``); the default is libps.so's kernels.
+    The multi-process CPU tests substitute a host implementation to check the
+    exchange logic under gloo."""
+
+    def __init__(self, scheme, n: int, lam: float, ring: int | None = None, dtype: str = "f64",
+                 arith: str = "ref", c: float = 1.0, group=None, device=None, compute=None,
+                 level_factory=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.P = dist.get_world_size(group)
+        self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
+        self.n, self.lam = int(n), float(lam)
+        self.tau = self.lam / self.n / c
+        R = self.spec.radius
+        self.R = R
+        self.ring = R if ring is None else int(ring)
+        grows = self.n + 1
+        self.grows = grows
+        self.plan = SlabPlan.build(grows, self.P, self.rank, R, periodic=False)
+        self.grid = nat.make_slab_grid(grows, grows, self.plan.row0, self.plan.rows, max(2, R),
+                                       self.ring, "dirichlet", dtype, arith)
+        make = level_factory or (lambda g: nat.Level(g, device=device))
+        self.levels = [make(self.grid) for _ in range(3)]
+        self.compute = compute or _KernelCompute(self.spec, self.lam, self.tau)
+        self.newest = None
+        self._streams = None
+
+    # -- transport ---------------------------------------------------------------------
+    def _p2p_ops(self, idx: int):
+        ops = []
+        lv = self.levels[idx]
+        for peer, first, count in self.plan.recvs:
+            ops.append(self.dist.P2POp(self.dist.irecv, rows_view(lv, first, count), peer,
+                                       self.group))
+        for peer, first, count in self.plan.sends:
+            ops.append(self.dist.P2POp(self.dist.isend, rows_view(lv, first, count), peer,
+                                       self.group))
+        return ops
+
+    def exchange(self, idx: int):
+        """Blocking (w.r.t. the current stream) halo exchange of level ``idx``."""
+        ops = self._p2p_ops(idx)
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    # -- time stepping -------------------------------------------------------------------
+    def load_initial(self, u0_rows: np.ndarray, v0_rows: np.ndarray):
+        """Upload this slab's own rows of u0 / v0, then exchange their halos."""
+        self.levels[1].upload(u0_rows)
+        self.levels[0].upload(v0_rows)
+        self.exchange(1)
+        self.exchange(0)
+
+    def first_step(self):
+        self.compute.first_step(self.grid, self.levels[1], self.levels[0], self.levels[2])
+        self.exchange(2)
+        self.newest = 2
+
+    def step(self, overlap: bool = True):
+        """One two-step update: boundary rows, then halo exchange on the communication
+        stream concurrently with the interior rows."""
+        cur = self.newest
+        nxt, prev = (cur + 1) % 3, (cur + 2) % 3
+        lv = self.levels
+        rows, R = self.plan.rows, self.R
+        c = self.compute
+        if self.P == 1 or rows < 3 * R or not overlap or not c.is_cuda:
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, rows)
+            self.exchange(nxt)
+        else:
+            import torch
+
+            if self._streams is None:
+                self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
+            comm, ev_edge, ev_comm = self._streams
+            main = torch.cuda.current_stream()
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, R)
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows)
+            ev_edge.record(main)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ev_edge)
+                self.exchange(nxt)
+                ev_comm.record(comm)
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], R, rows - R)
+            main.wait_event(ev_comm)
+        self.newest = nxt
+
+    def march(self, nsteps: int, overlap: bool = True):
+        for _ in range(nsteps):
+            self.step(overlap)
+
+    def own_rows(self, which: str = "newest") -> np.ndarray:
+        idx = self.newest if which == "newest" else (self.newest + 2) % 3
+        return self.levels[idx].download()
+
+
+class _KernelCompute:
+    """libps.so updates for a slab (the product path)."""
+
+    is_cuda = True
+
+    def __init__(self, spec, lam, tau):
+        self.t_u = nat.make_table(evaluate_table(spec.first_u, lam))
+        self.t_v = nat.make_table(evaluate_table(spec.first_v, lam))
+        self.t_two = nat.make_table(evaluate_table(spec.two_step, lam))
+        self.tau = tau
+
+    def first_step(self, grid, u0, v0, out):
+        nat.first_step(grid, u0, v0, out, self.t_u, self.t_v, self.tau)
+
+    def two_step_rows(self, grid, uk, ukm1, out, lo, hi):
+        if hi > lo:
+            nat.two_step_rows(grid, uk, ukm1, out, self.t_two, lo, hi)

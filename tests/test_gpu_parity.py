@@ -1,0 +1,323 @@
+"""GPU parity: libps.so's sm_100a kernels against the reference's golden vectors and the
+CPU oracle, bit for bit (fp64 and the reference's fp32 path) or within the stated
+tolerance (fp32 native vs the fp64 oracle).
+
+Every test calls through the C-ABI (via the drop-in simulator or the device API).
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="module")
+def ps():
+    import paper_1904_04048_b200 as mod
+
+    return mod
+
+
+@pytest.fixture(scope="module")
+def nat():
+    from paper_1904_04048_b200 import _native
+
+    return _native
+
+
+@pytest.fixture(scope="module")
+def runs():
+    with open(os.path.join(GOLD, "runs.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def fields():
+    return np.load(os.path.join(GOLD, "fields.npz"))
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    from oracle import oracle as O
+
+    O.lib()
+    return O
+
+
+def pairs(spec, role, lam):
+    from paper_1904_04048_b200.scheme import evaluate_table
+
+    return evaluate_table(getattr(spec, role), lam)
+
+
+def same_bits(a, b):
+    return a.dtype == b.dtype and a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+# ------------------------------------------------------------ golden single calls
+def test_dropin_two_step_and_first_step_match_reference_goldens(ps, runs, fields):
+    bad = []
+    for case in runs["cases"]:
+        spec = ps.named_scheme(case["scheme"])
+        key = case["key"]
+        a, b = fields[key + "_a"], fields[key + "_b"]
+        two = ps.two_step(a, b, spec, case["lam"], case["bc"])
+        first = ps.first_step(a, b, spec, case["lam"], case["tau"], case["bc"])
+        if not same_bits(two, fields[key + "_two"]):
+            bad.append(("two", key, float(np.abs(two - fields[key + "_two"]).max())))
+        if not same_bits(first, fields[key + "_first"]):
+            bad.append(("first", key, float(np.abs(first - fields[key + "_first"]).max())))
+    assert not bad, bad
+
+
+def test_dropin_run_matches_reference_marches(ps, runs, fields):
+    for m in runs["marches"]:
+        spec = ps.named_scheme(m["scheme"])
+        captured = []
+        rep = ps.run(ps.SimConfig(scheme=spec, n=m["n"], n_t=m["n_t"], lam=m["lam"], bc=m["bc"]),
+                     on_step=lambda k, f: captured.append(f))
+        assert same_bits(captured[m["mid_index"]], fields[m["key"] + "_mid"]), m["key"]
+        assert same_bits(captured[-1], fields[m["key"] + "_last"]), m["key"]
+        assert rep.error.hex() == m["error"], m["key"]
+        assert [e.hex() for e in rep.per_step_errors] == m["per_step"], m["key"]
+
+
+@pytest.mark.parametrize("table", [1, 2, 3])
+def test_paper_tables_match_reference(ps, runs, table):
+    from paper_1904_04048_b200.benchmarks import run_table
+
+    mine = run_table(table)
+    gold = runs["tables"][str(table)]
+    assert len(mine) == len(gold)
+    for r, g in zip(mine, gold):
+        for k, v in g.items():
+            if k.startswith("E_"):
+                assert r[k].hex() == v, (table, k, r[k], float.fromhex(v))
+
+
+def test_reference_property_suite(ps):
+    p5 = ps.named_scheme("P5")
+    ones = np.ones((9, 9))
+    assert ps.first_step(ones, np.zeros((9, 9)), p5, 0.6, 0.06, "periodic") == pytest.approx(ones, abs=1e-13)
+    assert ps.two_step(ones, ones, p5, 0.6, "periodic") == pytest.approx(ones, abs=1e-13)
+    rng = np.random.default_rng(3)
+    g = rng.normal(size=(9, 9))
+    out = ps.two_step(np.zeros((9, 9)), g, p5, 0.5, "periodic")
+    assert out[:8, :8] == pytest.approx(-g[:8, :8], abs=1e-14)
+    u_k, u_km1 = rng.normal(size=(9, 9)), rng.normal(size=(9, 9))
+    out = ps.two_step(u_k, u_km1, p5, 0.6, "dirichlet")
+    assert not out[0].any() and not out[-1].any() and not out[:, 0].any() and not out[:, -1].any()
+    captured = []
+    ps.run(ps.SimConfig(scheme=p5, n=12, n_t=6, lam=0.707), on_step=lambda k, f: captured.append(f))
+    assert all(np.abs(f - f.T).max() <= 1e-12 for f in captured)
+    errors = [ps.run(ps.SimConfig(scheme=p5, n=n, n_t=n, lam=0.707)).error for n in (10, 20, 40)]
+    assert errors[0] / errors[1] >= 8.0 and errors[1] / errors[2] >= 8.0
+    e_c5 = ps.run(ps.SimConfig(scheme=ps.named_scheme("C5"), n=10, n_t=1, lam=0.707)).error
+    e_c13 = ps.run(ps.SimConfig(scheme=ps.named_scheme("C13"), n=10, n_t=1, lam=0.707,
+                                bc="periodic")).error
+    assert e_c13 == pytest.approx(e_c5, rel=1e-12)
+    with pytest.warns(UserWarning, match="stable range"):
+        ps.run(ps.SimConfig(scheme=p5, n=8, n_t=2, lam=0.9))
+    zero = lambda x1, x2, *_: 0.0 * (x1 + x2)  # noqa: E731
+    with pytest.raises(ps.DegenerateNormError):
+        ps.run(ps.SimConfig(scheme=p5, n=8, n_t=3, lam=0.5, initial_u=zero, initial_v=zero,
+                            exact=zero))
+
+
+# ------------------------------------------------------------ streaming kernel vs oracle
+SHAPES = [("P5", 1), ("P9", 1), ("C9", 1), ("P13", 2)]
+
+
+@pytest.mark.parametrize("name,radius", SHAPES)
+@pytest.mark.parametrize("bc", ["dirichlet", "periodic"])
+@pytest.mark.parametrize("dtype,arith", [("f64", "ref"), ("f32", "ref"), ("f32", "native")])
+@pytest.mark.parametrize("n", [37, 600, 1031])
+def test_device_march_bitwise_vs_oracle(name, radius, bc, dtype, arith, n, oracle):
+    """Multi-strip, multi-chunk, ragged grids (n+1 not a multiple of the vector width)."""
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation(name, n, 0.4 if radius == 2 else 0.6, bc=bc, dtype=dtype, arith=arith)
+    rng = np.random.default_rng(n + radius)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    v0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    if bc == "periodic":
+        for f in (u0, v0):
+            f[:-1, -1] = f[:-1, 0]
+            f[-1, :] = f[0, :]
+    sim.load_initial(u0, v0)
+    sim.first_step()
+    sim.march(4)
+    got = sim.field()
+    ring = radius if bc == "dirichlet" else 0
+    o1 = oracle.first_step(u0, v0, pairs(sim.spec, "first_u", sim.lam),
+                           pairs(sim.spec, "first_v", sim.lam), sim.tau, bc, ring, arith)
+    want, _ = oracle.march(o1, u0, pairs(sim.spec, "two_step", sim.lam), 4, bc, ring, arith)
+    assert same_bits(got, want), float(np.abs(got.astype(float) - want).max())
+
+
+def test_generic_kernel_equals_streaming_kernel(ps, nat):
+    from paper_1904_04048_b200.device import Simulation
+
+    out = {}
+    for force in ("0", "1"):
+        os.environ["PS_FORCE_GENERIC"] = force
+        try:
+            sim = Simulation("P13", 700, 0.4, bc="periodic")
+            sim.gaussian_initial(16, 0.01, 0.05, seed=3)
+            sim.first_step()
+            sim.march(5)
+            out[force] = sim.field()
+        finally:
+            os.environ.pop("PS_FORCE_GENERIC", None)
+    assert same_bits(out["0"], out["1"])
+
+
+def test_two_step_in_place_over_previous_level(nat, oracle, ps):
+    """ps_two_step may write u^{k+1} over u^{k-1} (header contract)."""
+    n = 513
+    spec = ps.named_scheme("P9")
+    g = nat.make_grid(n + 1, n + 1, 2, 1, "dirichlet", "f64")
+    a, b = nat.Level(g), nat.Level(g)
+    rng = np.random.default_rng(9)
+    uk, ukm1 = rng.normal(size=(n + 1, n + 1)), rng.normal(size=(n + 1, n + 1))
+    a.upload(uk)
+    b.upload(ukm1)
+    t = nat.make_table(pairs(spec, "two_step", 0.6))
+    nat.two_step(g, a, b, b, t)
+    got = b.download()
+    want = oracle.two_step(uk, ukm1, pairs(spec, "two_step", 0.6), "dirichlet", 1)
+    assert same_bits(got, want)
+
+
+def test_row_range_and_virtual_slabs_bitwise(nat, oracle, ps):
+    """Row-slab decomposition on one device: P slabs with halo rows copied between
+    them give the single-grid result bit for bit."""
+    from paper_1904_04048_b200.slab import VirtualSlabs
+
+    n, steps = 777, 6
+    spec = ps.named_scheme("P13")
+    rng = np.random.default_rng(5)
+    u0 = rng.normal(size=(n + 1, n + 1))
+    v0 = rng.normal(size=(n + 1, n + 1))
+    o1 = oracle.first_step(u0, v0, pairs(spec, "first_u", 0.4), pairs(spec, "first_v", 0.4),
+                           0.4 / n, "dirichlet", 2)
+    want, _ = oracle.march(o1, u0, pairs(spec, "two_step", 0.4), steps, "dirichlet", 2)
+    for P in (1, 2, 3, 4, 8):
+        vs = VirtualSlabs(spec, n, 0.4, P, ring=2)
+        vs.load_initial(u0, v0)
+        vs.first_step()
+        vs.march(steps)
+        assert same_bits(vs.field(), want), P
+
+
+def test_gaussian_initial_data_matches_numpy(oracle):
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation("P13", 1023, 0.4, bc="dirichlet", dtype="f64")
+    pu, pv = sim.gaussian_initial(32, 0.01, 0.05, seed=0)
+    u0, v0 = sim.initial_fields()
+    ru = oracle.gaussian_sum(1023, pu[0], pu[1], pu[2])
+    rv = oracle.gaussian_sum(1023, pv[0], pv[1], pv[2])
+    # exp() may differ by an ulp between CUDA's libdevice and glibc; the sums agree to
+    # a few ulps of the field scale.
+    assert np.abs(u0 - ru).max() <= 1e-14 * max(1.0, np.abs(ru).max())
+    assert np.abs(v0 - rv).max() <= 1e-14 * max(1.0, np.abs(rv).max())
+
+
+# ------------------------------------------------------------ BASELINE configs
+def test_config1_full_run_bitwise(ps, oracle):
+    """C1: P5 Dirichlet 512^2 f64, λ=0.5, Gaussian u0, v0=0, 200 steps — whole run."""
+    from paper_1904_04048_b200.device import Simulation
+
+    n = 511
+    sim = Simulation("P5", n, 0.5, bc="dirichlet")
+    coords = np.arange(n + 1) / n
+    x1, x2 = np.meshgrid(coords, coords, indexing="ij")
+    u0 = np.exp(-((x1 - 0.5) ** 2 + (x2 - 0.5) ** 2) / (2 * 0.05**2))
+    sim.load_initial(u0, None)
+    sim.first_step()
+    sim.march(199)
+    o1 = oracle.first_step(u0, np.zeros_like(u0), pairs(sim.spec, "first_u", 0.5),
+                           pairs(sim.spec, "first_v", 0.5), sim.tau, "dirichlet", 1)
+    want, _ = oracle.march(o1, u0, pairs(sim.spec, "two_step", 0.5), 199, "dirichlet", 1)
+    assert same_bits(sim.field(), want)
+
+
+def test_config2_standing_wave(ps, oracle):
+    """C2: P9 periodic n=4096 f64 λ=0.6, standing wave m=4,k=6: 1000 steps; bitwise vs
+    the oracle over the first 60 steps, max-norm error vs the exact solution at 1000."""
+    from paper_1904_04048_b200.device import Simulation
+
+    n = 4096
+    sim = Simulation("P9", n, 0.6, bc="periodic")
+    omega = sim.standing_wave_initial(4, 6)
+    u0, v0 = sim.initial_fields()
+    sim.first_step()
+    sim.march(59)
+    o1 = oracle.first_step(u0, v0, pairs(sim.spec, "first_u", 0.6),
+                           pairs(sim.spec, "first_v", 0.6), sim.tau, "periodic", 0)
+    want, _ = oracle.march(o1, u0, pairs(sim.spec, "two_step", 0.6), 59, "periodic", 0)
+    assert same_bits(sim.field(), want)
+    sim.march(1000 - 60)
+    t = 1000 * sim.tau
+    coords = np.arange(n + 1) / n
+    x1, x2 = np.meshgrid(coords, coords, indexing="ij")
+    exact = np.sin(2 * np.pi * 4 * x1) * np.sin(2 * np.pi * 6 * x2) * (
+        np.cos(omega * t) + np.sin(omega * t))
+    err = np.abs(sim.field() - exact).max()
+    assert err < 1e-3, err
+
+
+def test_config3_f32_native_within_tolerance_of_f64(oracle):
+    """C3 shape (P13, ring 2, λ=0.4, Gaussian u0/v0) at a reduced size: f32 native vs
+    the f64 run after 100 steps, relative max-norm <= 1e-4."""
+    from paper_1904_04048_b200.device import Simulation
+
+    res = {}
+    for dt, ar in (("f64", "ref"), ("f32", "native"), ("f32", "ref")):
+        sim = Simulation("P13", 2047, 0.4, bc="dirichlet", dtype=dt, arith=ar)
+        sim.gaussian_initial(32, 0.01, 0.05, seed=0)
+        sim.first_step()
+        sim.march(99)
+        res[(dt, ar)] = sim.field().astype(np.float64)
+    ref = res[("f64", "ref")]
+    scale = np.abs(ref).max()
+    for key in (("f32", "native"), ("f32", "ref")):
+        rel = np.abs(res[key] - ref).max() / scale
+        assert rel <= 1e-4, (key, rel)
+
+
+def test_config4_full_size_slab_check(oracle):
+    """C4 at full size (P9, ring 1, 32768^2 f64, λ=0.6, 64 Gaussians, v0=0): after a few
+    steps, one step over a band of rows is checked bitwise against the oracle run on
+    the downloaded neighbourhood (a size-independent exact check)."""
+    import torch
+
+    from paper_1904_04048_b200.device import Simulation
+
+    n = 32767
+    sim = Simulation("P9", n, 0.6, bc="dirichlet")
+    sim.gaussian_initial(64, 0.01, 0.05, seed=0, v_zero=True)
+    sim.first_step()
+    sim.march(3)
+    uk_lv = sim.levels[sim.newest]
+    ukm1_lv = sim.levels[(sim.newest + 2) % 3]
+    band = slice(16380 - 1, 16420 + 1)
+    uk = uk_lv.view()[band].cpu().numpy()
+    ukm1 = ukm1_lv.view()[band].cpu().numpy()
+    sim.march(1)
+    got = sim.levels[sim.newest].view()[16380:16420].cpu().numpy()
+    want = oracle.two_step(uk, ukm1, pairs(sim.spec, "two_step", 0.6), "dirichlet", 1)[1:-1]
+    # the band's first/last columns are the global ring (zero in both)
+    assert same_bits(got, want)
+    torch.cuda.synchronize()
