@@ -18,7 +18,9 @@
  *     periodic grids hold the n x n independent nodes; the reference's alias row/col n
  *     is the first image row/col.
  *   - Calls are asynchronous on the given stream (NULL = legacy default stream), never
- *     allocate, keep no global mutable state, and are safe from concurrent threads.
+ *     allocate device memory, and are safe from concurrent threads.  The only library
+ *     state is a mutex-guarded cache of instantiated CUDA graphs (ps_march) and the
+ *     per-launch tile counters of the streaming kernel.
  *   - Return 0 (PS_OK) or a distinct ps_status; ps_strerror() names it.
  */
 #ifndef PS_H_
@@ -136,7 +138,9 @@ ps_status ps_two_step_rows(const ps_grid* g, const void* uk, const void* ukm1, v
 
 /* nsteps two-step updates rotating three levels in place (the loop of run(),
  * simulator.py:271-274).  On entry lvl[*newest] = u^k and lvl[(*newest+2)%3] = u^{k-1};
- * on return *newest names the level holding the last update. */
+ * on return *newest names the level holding the last update.  For nsteps >= 6 one
+ * rotation cycle (3 launches) is captured into a CUDA graph once and replayed
+ * (environment PS_GRAPH=0 disables). */
 ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
                    int32_t* newest, void* stream);
 

@@ -15,7 +15,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libps.so")
+# PS_LIBRARY points at an alternative build (tuning variants); default: the in-tree .so
+LIB_PATH = os.environ.get("PS_LIBRARY") or os.path.join(_HERE, "libps.so")
 
 PS_MAX_TAPS = 32
 BC = {"dirichlet": 0, "periodic": 1}

@@ -24,9 +24,25 @@
 #include "ps_arith.cuh"
 #include "ps_ptx.cuh"
 
+// Streaming-kernel geometry (tuning builds override with -D): consumer warps per
+// block, rows per pipeline stage for radius 1 / radius 2, pipeline stages.
+#ifndef PS_NW
+#define PS_NW 8
+#endif
+#ifndef PS_RB1
+#define PS_RB1 4
+#endif
+#ifndef PS_RB2
+#define PS_RB2 4
+#endif
+#ifndef PS_NS
+#define PS_NS 3
+#endif
+
 namespace ps {
 
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<uint64_t> g_launch_seq{0};
 
 // ---------------------------------------------------------------------------
 // Stencil shapes: compile-time tap lists in the reference's dict order
@@ -107,12 +123,19 @@ struct StreamGeom {
   static constexpr int W = NW * 32 * V;  // columns per strip
   static constexpr int SU = W + 2 * V;   // u^k slot: strip + one 16-byte vector each side
   static constexpr size_t smem_bytes =
-      size_t(NS) * RB * (SU + W) * sizeof(T) + 2 * NS * sizeof(uint64_t);
+      size_t(NS) * RB * (SU + W) * sizeof(T) + 2 * NS * sizeof(uint64_t) + 2 * NS * sizeof(int);
 };
+
+// Dynamic tile scheduler: one counter pair per in-flight launch (slot = launch
+// sequence number mod kSlots).  The last block to finish resets its slot, so the next
+// launch that reuses it (kSlots launches later) starts from zero.
+constexpr int kSlots = 1024;
+__device__ unsigned int g_tile_next[kSlots];
+__device__ unsigned int g_tile_done[kSlots];
 
 template <typename T, int A, class S, bool PER, int NW, int RB, int NS>
 __global__ void __launch_bounds__((NW + 1) * 32)
-    k_two_step_stream(const __grid_constant__ StreamParams p) {
+    k_two_step_stream(const __grid_constant__ StreamParams p, const int slot) {
   using G = StreamGeom<T, NW, RB, NS>;
   constexpr int V = G::V, W = G::W, SU = G::SU;
   constexpr int R = S::R;
@@ -127,6 +150,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   T* s_km = s_uk + NS * RB * SU;
   uint64_t* full = reinterpret_cast<uint64_t*>(s_km + NS * RB * W);
   uint64_t* empty = full + NS;
+  int* s_tile = reinterpret_cast<int*>(empty + NS);  // tile of each stage (-1: stop)
+  int* s_mlo = s_tile + NS;                           // first window row of each stage
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -147,9 +172,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   if (warp == NW) {
     // ---------------- producer: one elected lane streams rows via TMA ----------
     if (lane == 0) {
-      const uint64_t pol = l2_policy_evict_first();
+      // u^k rows are re-read as halos by the neighbouring tiles: keep them normal in
+      // L2; u^{k-1} is read exactly once: evict first.
+      const uint64_t pol_uk = l2_policy_evict_normal();
+      const uint64_t pol_km = l2_policy_evict_first();
       uint32_t g = 0;
-      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      int tile = blockIdx.x;
+      while (tile < p.ntiles) {
         const int chunk = tile / p.nstrips;
         const int strip = tile - chunk * p.nstrips;
         const int i0 = p.rlo + chunk * p.rc;
@@ -163,20 +192,34 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           const uint32_t s = g % NS;
           const uint32_t k = g / NS;
           if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+          s_tile[s] = tile;
+          s_mlo[s] = mlo;
           const int mhi = min(mlo + RB, ne);
           const int nk = max(0, mhi - max(mlo, 2 * R));
           mbar_arrive_expect_tx(&full[s], uint32_t(mhi - mlo) * ukb + uint32_t(nk) * kmb);
           for (int m = mlo; m < mhi; ++m) {
             const int64_t e = int64_t(i0) - R + m;
             tma_load_1d(s_uk + (s * RB + (m - mlo)) * SU, uk + e * pitch + j0 - V, ukb, &full[s],
-                        pol);
+                        pol_uk);
             if (m >= 2 * R) {
               const int64_t i = int64_t(i0) + m - 2 * R;
               tma_load_1d(s_km + (s * RB + (m - mlo)) * W, ukm1 + i * pitch + j0, kmb, &full[s],
-                          pol);
+                          pol_km);
             }
           }
         }
+        tile = int(gridDim.x + atomicAdd(&g_tile_next[slot], 1u));
+      }
+      // sentinel stage: tells the consumers to stop
+      const uint32_t s = g % NS;
+      const uint32_t k = g / NS;
+      if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+      s_tile[s] = -1;
+      mbar_arrive(&full[s]);
+      __threadfence();
+      if (atomicAdd(&g_tile_done[slot], 1u) == gridDim.x - 1) {
+        g_tile_next[slot] = 0;
+        g_tile_done[slot] = 0;
       }
     }
     return;
@@ -198,9 +241,9 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     for (int x = 0; x < 3 * V; ++x) w[r][x] = T(0);
 
   const int tcol = threadIdx.x * V;
-  uint32_t g = 0;
 
-  auto row_step = [&](const T* su_row, const T* sk_row, int m, int i0, int jv, bool active) {
+  auto row_step = [&](const T* su_row, const T* sk_row, int m, int i0, int jv, bool active,
+                      bool cols_inner) {
     // slide the window and admit u^k row (i0 - R + m)
 #pragma unroll
     for (int r = 0; r < 2 * R; ++r)
@@ -227,20 +270,25 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       for (int s = 0; s < S::N; ++s) a = Ar::tap(a, c[s], w[R + S::q(s, 0)][V + v + S::q(s, 1)]);
       acc[v] = a;
     }
+    T* dst = ukp1 + int64_t(i) * pitch + jv;
     if constexpr (PER) {
 #pragma unroll
       for (int v = 0; v < V; ++v) out[v] = Ar::two(acc[v], km[v]);
     } else {
       const int gi = p.row0 + i;
       const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
+      if (row_in && cols_inner) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int j = jv + v;
-        const bool in = row_in && (j >= p.ring) && (j < p.cols - p.ring);
-        out[v] = in ? Ar::two(acc[v], km[v]) : T(0);
+        for (int v = 0; v < V; ++v) out[v] = Ar::two(acc[v], km[v]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int j = jv + v;
+          const bool in = row_in && (j >= p.ring) && (j < p.cols - p.ring);
+          out[v] = in ? Ar::two(acc[v], km[v]) : T(0);
+        }
       }
     }
-    T* dst = ukp1 + int64_t(i) * pitch + jv;
     if (jv + V <= p.cols) {
       *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(out);
     } else {
@@ -270,7 +318,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
   };
 
-  for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+  for (uint32_t g = 0;; ++g) {
+    const uint32_t s = g % NS;
+    const uint32_t k = g / NS;
+    mbar_wait(&full[s], k & 1);
+    const int tile = s_tile[s];
+    if (tile < 0) break;
+    const int mlo = s_mlo[s];
     const int chunk = tile / p.nstrips;
     const int strip = tile - chunk * p.nstrips;
     const int i0 = p.rlo + chunk * p.rc;
@@ -278,23 +332,20 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     const int j0 = strip * W;
     const int jv = j0 + tcol;
     const bool active = jv < p.cols;
+    const bool cols_inner = (j0 >= p.ring) && (j0 + W <= p.cols - p.ring);
     const int ne = (i1 - i0) + 2 * R;
-    for (int mlo = 0; mlo < ne; mlo += RB, ++g) {
-      const uint32_t s = g % NS;
-      const uint32_t k = g / NS;
-      mbar_wait(&full[s], k & 1);
-      const T* su = s_uk + s * RB * SU;
-      const T* sk = s_km + s * RB * W;
-      if (mlo + RB <= ne) {
+    const T* su = s_uk + s * RB * SU;
+    const T* sk = s_km + s * RB * W;
+    if (mlo + RB <= ne) {
 #pragma unroll
-        for (int mm = 0; mm < RB; ++mm) row_step(su + mm * SU, sk + mm * W, mlo + mm, i0, jv, active);
-      } else {
-        for (int mm = 0; mm < ne - mlo; ++mm)
-          row_step(su + mm * SU, sk + mm * W, mlo + mm, i0, jv, active);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      for (int mm = 0; mm < RB; ++mm)
+        row_step(su + mm * SU, sk + mm * W, mlo + mm, i0, jv, active, cols_inner);
+    } else {
+      for (int mm = 0; mm < ne - mlo; ++mm)
+        row_step(su + mm * SU, sk + mm * W, mlo + mm, i0, jv, active, cols_inner);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -560,9 +611,9 @@ static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, 
 template <typename T, int A, class S, bool PER>
 static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
                                const ps_table* t, int64_t rlo, int64_t rhi, cudaStream_t st) {
-  constexpr int NW = 4;
-  constexpr int RB = (S::R == 1) ? 6 : 5;
-  constexpr int NS = 4;
+  constexpr int NW = PS_NW;
+  constexpr int RB = (S::R == 1) ? PS_RB1 : PS_RB2;
+  constexpr int NS = PS_NS;
   using Gm = StreamGeom<T, NW, RB, NS>;
   auto kern = k_two_step_stream<T, A, S, PER, NW, RB, NS>;
   static std::once_flag once;
@@ -597,12 +648,13 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
   int rc = env_int("PS_ROW_CHUNK", 0);
   if (rc <= 0) {
-    // Enough tiles that the static round-robin leaves <1% imbalance, but tall enough
-    // that re-reading 2R halo rows per tile stays negligible.
-    const int64_t want_tiles = int64_t(resident) * 64;
-    int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
+    // Tiles are claimed dynamically, so balance only needs ~8 tiles per resident block;
+    // taller tiles re-read fewer halo rows (2R per tile).  128 rows keeps the tail
+    // under one ~25 us tile on the big grids; medium grids drop to >= 16 rows.
+    const int64_t want_tiles = int64_t(resident) * 8;
+    const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
     rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
-    rc = std::max(rc, 8 * S::R);
+    rc = std::max(rc, std::max(16, 8 * S::R));
     rc = std::min(rc, 128);
   }
   rc = int(std::min<int64_t>(rc, nrows));
@@ -610,7 +662,8 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   const int64_t nchunks = (nrows + rc - 1) / rc;
   p.ntiles = int32_t(nchunks * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
-  kern<<<grid, (NW + 1) * 32, Gm::smem_bytes, st>>>(p);
+  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  kern<<<grid, (NW + 1) * 32, Gm::smem_bytes, st>>>(p, slot);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return last_cuda_status();
 }
@@ -652,6 +705,82 @@ static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ---------------------------------------------------------------------------
+// CUDA-graph replay of the march: one rotation cycle (3 two-step launches) is
+// captured once per (grid, levels, table, phase) and replayed nsteps/3 times, which
+// removes per-launch CPU cost and launch gaps on latency-bound grids.
+// ---------------------------------------------------------------------------
+struct GraphKey {
+  ps_grid g;
+  void* lvl[3];
+  int32_t cur;
+  int32_t dev;
+  ps_table t;
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec;
+};
+static std::mutex g_graph_mu;
+static GraphEntry g_graphs[32];
+static int g_ngraphs = 0;
+static int g_graph_next = 0;
+
+static cudaStream_t capture_stream(int dev) {
+  static cudaStream_t streams[64] = {};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
+static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, const ps_table* t) {
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.g = *g;
+  for (int x = 0; x < 3; ++x) key.lvl[x] = lvl[x];
+  key.cur = cur;
+  cudaGetDevice(&key.dev);
+  key.t.ntaps = t->ntaps;
+  for (int s = 0; s < t->ntaps; ++s) {
+    key.t.q1[s] = t->q1[s];
+    key.t.q2[s] = t->q2[s];
+    key.t.c[s] = t->c[s];
+  }
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  for (int e = 0; e < g_ngraphs; ++e)
+    if (std::memcmp(&g_graphs[e].key, &key, sizeof(key)) == 0) return g_graphs[e].exec;
+  cudaStream_t cs = capture_stream(key.dev);
+  if (!cs) return nullptr;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  int c = cur;
+  ps_status st = PS_OK;
+  for (int k = 0; k < 3 && st == PS_OK; ++k) {
+    st = two_step_impl(g, lvl[c], lvl[(c + 2) % 3], lvl[(c + 1) % 3], t, 0, g->rows, cs);
+    c = (c + 1) % 3;
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (st != PS_OK || ec != cudaSuccess || !graph ||
+      cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return nullptr;
+  }
+  cudaGraphDestroy(graph);
+  g_launches.fetch_sub(3, std::memory_order_relaxed);  // captured, not executed
+  GraphEntry& slot = g_graphs[g_graph_next];
+  if (g_graph_next < g_ngraphs && slot.exec) cudaGraphExecDestroy(slot.exec);
+  slot.key = key;
+  slot.exec = exec;
+  g_graph_next = (g_graph_next + 1) % 32;
+  g_ngraphs = std::min(g_ngraphs + 1, 32);
+  return exec;
+}
 
 }  // namespace ps
 
@@ -837,7 +966,17 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
     if (!aligned16(lvl[x])) return PS_ERR_ALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int cur = *newest;
-  for (int64_t k = 0; k < nsteps; ++k) {
+  int64_t k = 0;
+  if (nsteps >= 6 && env_int("PS_GRAPH", 1) != 0) {
+    if (cudaGraphExec_t exec = cycle_graph(g, lvl, cur, t)) {
+      for (; k + 3 <= nsteps; k += 3) {
+        if (cudaGraphLaunch(exec, st) != cudaSuccess) return PS_ERR_CUDA;
+        g_launches.fetch_add(3, std::memory_order_relaxed);
+      }
+      // a full cycle returns the rotation to the same phase: cur is unchanged
+    }
+  }
+  for (; k < nsteps; ++k) {
     const int prev = (cur + 2) % 3;
     const int next = (cur + 1) % 3;
     if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st)) != PS_OK)
