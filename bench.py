@@ -229,12 +229,12 @@ def reference_arm(args, cfg, cfg_name):
 
 
 # ------------------------------------------------------------------------------ GPU arm
-def make_sim(cfg):
+def make_sim(cfg, tsteps=1):
     from paper_1904_04048_b200.device import Simulation
 
     sim = Simulation(cfg["scheme"], cfg["n"], cfg["lam"], bc=cfg["bc"],
                      ring=cfg["ring"] if cfg["bc"] == "dirichlet" else None,
-                     dtype=cfg["dtype"], arith=cfg["arith"])
+                     dtype=cfg["dtype"], arith=cfg["arith"], tsteps=tsteps)
     ic = cfg["ic"]
     if ic == "standing":
         sim.standing_wave_initial(4, 6)
@@ -259,7 +259,8 @@ def gpu_arm_single(args, cfg, cfg_name):
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    sim = make_sim(cfg)
+    T = args.tsteps
+    sim = make_sim(cfg, T)
     sim.first_step()
     stream = torch.cuda.current_stream()
     # warm-up also instantiates ps_march's CUDA graph (captured for runs of >= 6 steps)
@@ -268,7 +269,10 @@ def gpu_arm_single(args, cfg, cfg_name):
     torch.cuda.synchronize()
 
     lup_step = sim.updated_nodes
-    bytes_launch = 3 * sim.itemsize * lup_step
+    # algorithmic HBM words per update: 3 (read u^k, u^{k-1}; write u^{k+1}); with
+    # temporal blocking depth T one launch reads 2 levels and writes 2 for T updates
+    words_per_lup = 3.0 if T == 1 else 4.0 / T
+    bytes_launch = words_per_lup * T * sim.itemsize * lup_step
     K = args.steps
     t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = nat.launch_count()
@@ -280,8 +284,9 @@ def gpu_arm_single(args, cfg, cfg_name):
         torch.cuda.synchronize()
     launches = nat.launch_count() - launches0
     total_ms = t_begin.elapsed_time(t_end)
-    # the timed region holds only the K hot-kernel launches, back to back
-    avg_launch_ms = total_ms / K
+    # the timed region holds only the hot-kernel launches, back to back (K/T launches of
+    # T fused updates each)
+    avg_launch_ms = total_ms / K * T
     value = lup_step * K / (total_ms * 1e-3) / 1e9
     peak, peak_src = load_peak()
     achieved = bytes_launch / (avg_launch_ms * 1e-3) / 1e9
@@ -294,7 +299,7 @@ def gpu_arm_single(args, cfg, cfg_name):
         "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
         "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
                    "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
-                   "parallelism": "single GPU",
+                   "parallelism": "single GPU", "temporal_blocking": T,
                    "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
                          "3 levels streamed per step" if sim.level_bytes > 126e6 else
                          "grid fits in L2 (latency-bound correctness config)"},
@@ -303,7 +308,7 @@ def gpu_arm_single(args, cfg, cfg_name):
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_launch,
                      "kernel_ms_per_launch": avg_launch_ms,
-                     "lup_per_launch": lup_step, "bytes_per_lup": 3 * sim.itemsize},
+                     "lup_per_launch": lup_step * T, "bytes_per_lup": words_per_lup * sim.itemsize},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }
@@ -459,6 +464,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--tsteps", type=int, default=1, choices=(1, 2, 4),
+                    help="temporal blocking depth (Dirichlet configs)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

@@ -144,6 +144,20 @@ ps_status ps_two_step_rows(const ps_grid* g, const void* uk, const void* ukm1, v
 ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
                    int32_t* newest, void* stream);
 
+/* Temporal blocking: tsteps (2 or 4) two-step updates fused into one
+ * streaming pass over u^k / u^{k-1}; writes only u^{k+tsteps-1} (out_prev) and
+ * u^{k+tsteps} (out_last).  HBM traffic 4/tsteps words per update instead of 3.
+ * Dirichlet grids, shapes P5/P9/C9/P13; results bitwise equal to tsteps ps_two_step
+ * calls.  The four buffers must be distinct. */
+ps_status ps_two_step_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
+                         void* out_last, const ps_table* t, int32_t tsteps, void* stream);
+
+/* nsteps updates over four rotating levels with temporal blocking depth tsteps (1, 2, 4);
+ * lvl[*newest] = u^k and lvl[*previous] = u^{k-1} on entry and on return.  nsteps not
+ * divisible by tsteps finishes with single steps. */
+ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
+                      int32_t tsteps, int32_t* newest, int32_t* previous, void* stream);
+
 /* Sum of K isotropic Gaussians sampled at x1 = i/n, x2 = j/n (the reference's node
  * coordinates np.arange(n+1)/n, simulator.py:254-255) in f64, k order:
  *   u = sum_k amp[k] * exp(-((x1-cx[k])^2 + (x2-cy[k])^2) / (2*(width[k]^2)))

@@ -50,7 +50,7 @@ class PsTable(ctypes.Structure):
 
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
-           "ps_march",
+           "ps_march", "ps_two_step_tb", "ps_march_tb",
            "ps_gaussian_sum", "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
@@ -82,6 +82,9 @@ def load_library(path: str = LIB_PATH):
             "ps_two_step": (i32, [G, vp, vp, vp, T, vp]),
             "ps_two_step_rows": (i32, [G, vp, vp, vp, T, i64, i64, vp]),
             "ps_march": (i32, [G, ctypes.POINTER(vp), i64, T, ctypes.POINTER(i32), vp]),
+            "ps_two_step_tb": (i32, [G, vp, vp, vp, vp, T, i32, vp]),
+            "ps_march_tb": (i32, [G, ctypes.POINTER(vp), i64, T, i32, ctypes.POINTER(i32),
+                                  ctypes.POINTER(i32), vp]),
             "ps_gaussian_sum": (i32, [G, vp, i32, vp, vp, vp, vp, i64, vp]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
@@ -220,6 +223,23 @@ def march(grid, levels, nsteps: int, t: PsTable, newest: int, stream=None) -> in
     check(load_library().ps_march(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
                                   ctypes.byref(nw), stream or current_stream()), "ps_march")
     return nw.value
+
+
+def two_step_tb(grid, uk: Level, ukm1: Level, out_prev: Level, out_last: Level, t: PsTable,
+                tsteps: int, stream=None):
+    check(load_library().ps_two_step_tb(ctypes.byref(grid), uk.ptr, ukm1.ptr, out_prev.ptr,
+                                        out_last.ptr, ctypes.byref(t), int(tsteps),
+                                        stream or current_stream()), "ps_two_step_tb")
+
+
+def march_tb(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, previous: int,
+             stream=None) -> tuple[int, int]:
+    arr = (ctypes.c_void_p * 4)(*[lv.ptr.value for lv in levels])
+    nw, pv = ctypes.c_int32(newest), ctypes.c_int32(previous)
+    check(load_library().ps_march_tb(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
+                                     int(tsteps), ctypes.byref(nw), ctypes.byref(pv),
+                                     stream or current_stream()), "ps_march_tb")
+    return nw.value, pv.value
 
 
 def gaussian_sum(grid, level: Level, centres, widths, amps, n: int, stream=None):

@@ -349,6 +349,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   }
 }
 
+#include "ps_tblock.cuh"
+
 // ---------------------------------------------------------------------------
 // Generic kernels (any tap list within the ghost width; first step; images)
 // ---------------------------------------------------------------------------
@@ -707,6 +709,115 @@ static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ---------------------------------------------------------------------------
+// Temporal blocking (ps_tblock.cuh)
+// ---------------------------------------------------------------------------
+#ifndef PS_TB_NW
+#define PS_TB_NW 4
+#endif
+#ifndef PS_TB_RB
+#define PS_TB_RB 4
+#endif
+#ifndef PS_TB_NS
+#define PS_TB_NS 4
+#endif
+
+template <typename T, int A, class S, int TS>
+static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
+                           void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
+                           cudaStream_t st) {
+  constexpr int NW = PS_TB_NW, RB = PS_TB_RB, NS = PS_TB_NS;
+  using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
+  auto kern = k_two_step_tb<T, A, S, TS, NW, RB, NS>;
+  static std::once_flag once;
+  static int blocks_per_sm = 1;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, (NW + 1) * 32,
+                                                  Gm::smem_bytes);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  });
+  const int64_t nrows = rhi - rlo;
+  if (nrows <= 0) return PS_OK;
+  TBParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.uk = at_origin<T>(g, uk);
+  p.ukm1 = at_origin<T>(g, ukm1);
+  p.out_prev = at_origin<T>(g, out_prev);
+  p.out_last = at_origin<T>(g, out_last);
+  p.pitch = g->pitch;
+  p.rows = int32_t(g->rows);
+  p.cols = int32_t(g->cols);
+  p.ring = g->ring;
+  p.row0 = int32_t(g->row0);
+  p.grows = int32_t(g->grows);
+  p.rlo = int32_t(rlo);
+  p.rhi = int32_t(rhi);
+  p.gmin = -int32_t(g->ghost);
+  p.gmax = int32_t(g->rows + g->ghost);
+  p.cmax = int32_t(g->pitch - (g->origin - g->ghost * g->pitch));
+  for (int s = 0; s < S::N; ++s) {
+    p.c[s] = t->c[s];
+    p.cf[s] = static_cast<float>(t->c[s]);
+  }
+  const int resident = std::max(1, dev_info().nsm) * blocks_per_sm;
+  p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
+  int rc = env_int("PS_TB_ROW_CHUNK", 0);
+  if (rc <= 0) {
+    const int64_t want_tiles = int64_t(resident) * 8;
+    const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
+    rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
+    rc = std::max(rc, std::max(32, 8 * S::R * TS));
+    rc = std::min(rc, 256);
+  }
+  rc = int(std::min<int64_t>(rc, nrows));
+  p.rc = rc;
+  p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
+  const int grid = int(std::min<int64_t>(p.ntiles, resident));
+  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  kern<<<grid, (NW + 1) * 32, Gm::smem_bytes, st>>>(p, slot);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return last_cuda_status();
+}
+
+template <typename T, int A, int TS>
+static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
+                             void* ol, const ps_table* t, cudaStream_t st) {
+  if (shape_matches<ShapeP5>(t))
+    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+  if (shape_matches<ShapeP9>(t))
+    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+  if (shape_matches<ShapeC9>(t))
+    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+  if (shape_matches<ShapeP13>(t))
+    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+  return PS_ERR_TABLE;
+}
+
+template <int TS>
+static ps_status tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol,
+                         const ps_table* t, cudaStream_t st) {
+  if (g->dtype == PS_F64) return dispatch_tb<double, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, st);
+  if (g->arith == PS_ARITH_NATIVE)
+    return dispatch_tb<float, ARITH_NATIVE, TS>(g, uk, ukm1, op, ol, t, st);
+  return dispatch_tb<float, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, st);
+}
+
+static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op,
+                                  void* ol, const ps_table* t, int tsteps, cudaStream_t st) {
+  switch (tsteps) {
+    case 2: return tb_impl<2>(g, uk, ukm1, op, ol, t, st);
+    case 4: return tb_impl<4>(g, uk, ukm1, op, ol, t, st);
+    default: return PS_ERR_ARG;
+  }
+}
+
+static bool tb_supported(const ps_grid* g, const ps_table* t) {
+  return g->bc == PS_BC_DIRICHLET && g->rows >= 4 && g->cols >= 4 &&
+         (shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) || shape_matches<ShapeC9>(t) ||
+          shape_matches<ShapeP13>(t));
+}
+
+// ---------------------------------------------------------------------------
 // CUDA-graph replay of the march: one rotation cycle (3 two-step launches) is
 // captured once per (grid, levels, table, phase) and replayed nsteps/3 times, which
 // removes per-launch CPU cost and launch gaps on latency-bound grids.
@@ -984,6 +1095,63 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
     cur = next;
   }
   *newest = cur;
+  return PS_OK;
+}
+
+ps_status ps_two_step_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
+                         void* out_last, const ps_table* t, int32_t tsteps, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!uk || !ukm1 || !out_prev || !out_last) return PS_ERR_ARG;
+  if (out_prev == uk || out_prev == ukm1 || out_last == uk || out_last == ukm1 ||
+      out_prev == out_last)
+    return PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  if (!tb_supported(g, t)) return PS_ERR_ARG;
+  if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(out_prev) || !aligned16(out_last))
+    return PS_ERR_ALIGN;
+  return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
+                          static_cast<cudaStream_t>(stream));
+}
+
+ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
+                      int32_t tsteps, int32_t* newest, int32_t* previous, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!lvl || !newest || !previous || nsteps < 0) return PS_ERR_ARG;
+  int cur = *newest, prev = *previous;
+  if (cur < 0 || cur > 3 || prev < 0 || prev > 3 || cur == prev) return PS_ERR_ARG;
+  for (int x = 0; x < 4; ++x)
+    if (!lvl[x] || !aligned16(lvl[x])) return lvl[x] ? PS_ERR_ALIGN : PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  if (tsteps != 1 && tsteps != 2 && tsteps != 4) return PS_ERR_ARG;
+  if (tsteps > 1 && !tb_supported(g, t)) return PS_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t k = 0;
+  auto free_pair = [&](int a, int b, int* f1, int* f2) {
+    int n = 0;
+    for (int x = 0; x < 4; ++x)
+      if (x != a && x != b) (n++ == 0 ? *f1 : *f2) = x;
+  };
+  if (tsteps > 1) {
+    for (; k + tsteps <= nsteps; k += tsteps) {
+      int f1, f2;
+      free_pair(cur, prev, &f1, &f2);
+      if ((s = two_step_tb_impl(g, lvl[cur], lvl[prev], lvl[f1], lvl[f2], t, tsteps, st)) != PS_OK)
+        return s;
+      prev = f1;
+      cur = f2;
+    }
+  }
+  for (; k < nsteps; ++k) {
+    int f1, f2;
+    free_pair(cur, prev, &f1, &f2);
+    if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[f1], t, 0, g->rows, st)) != PS_OK) return s;
+    prev = cur;
+    cur = f1;
+  }
+  *newest = cur;
+  *previous = prev;
   return PS_OK;
 }
 

@@ -1,0 +1,304 @@
+// ps_tblock.cuh — temporal blocking: TS two-step updates fused in one streaming pass
+// (BASELINE config 5, T in {2, 4}).  Included by ps_device.cu.
+//
+// One pass reads u^k and u^{k-1} once and writes only the last two levels u^{k+TS-1}
+// and u^{k+TS}: HBM traffic falls from 3 words per update to 4/TS (+ halos).
+//
+// Same producer/consumer skeleton as k_two_step_stream (TMA bulk row copies into an
+// mbarrier ring, dynamic tiles).  The difference is in the consumers:
+//   * each WARP is an independent column unit of 32 vectors (32*V columns) whose
+//     outputs are valid on the centre WO = 32V - 2HT columns (HT = R*(TS-1) rounded up
+//     to a vector); neighbouring warps overlap by 2HT columns, so no cross-warp exchange
+//     is ever needed — the halo is recomputed instead of communicated;
+//   * stage t (1..TS) keeps a (2R+1)-row register window of level k+t-1 and produces
+//     level k+t R rows behind stage t-1; the -u^{k+t-2} term is the oldest row of the
+//     window two stages down (stage 1 takes u^{k-1} from shared memory);
+//   * horizontal neighbours of stage outputs come from the adjacent lanes by shuffle;
+//   * every stage re-pins the Dirichlet ring (and zeroes rows/cols outside the grid),
+//     so each intermediate level is exactly what TS separate launches would produce —
+//     results are bitwise equal to the unblocked march.
+// Dirichlet grids only (periodic images would need per-level wrap handling).
+#pragma once
+// (included inside namespace ps, after the streaming kernel's helpers)
+
+struct TBParams {
+  const void* uk;
+  const void* ukm1;
+  void* out_prev;  // u^{k+TS-1}
+  void* out_last;  // u^{k+TS}
+  int64_t pitch;
+  int32_t rows, cols, ring, row0, grows;
+  int32_t rlo, rhi;        // rows this launch finalises
+  int32_t gmin, gmax;      // loadable row range [gmin, gmax) (allocation incl. ghosts)
+  int32_t cmax;            // loadable columns: element index < cmax (from logical col 0)
+  int32_t nstrips, rc, ntiles;
+  double c[PS_MAX_TAPS];
+  float cf[PS_MAX_TAPS];
+};
+
+template <typename T, int NW, int RB, int NS, int R, int TS>
+struct TBGeom {
+  static constexpr int V = Vec<T>::V;
+  // Column halo per side.  Stage 1 reads true neighbours from shared memory; each later
+  // stage loses R valid columns at each warp edge, so R*(TS-1) (rounded to a vector).
+  static constexpr int HT = ((R * (TS - 1) + V - 1) / V) * V;
+  static constexpr int WO = 32 * V - 2 * HT;              // valid output columns per warp
+  static constexpr int W = NW * WO;                        // output columns per block strip
+  static constexpr int LU = W + 2 * HT + 2 * V;            // u^k row slot (extra vec each side)
+  static constexpr int LK = W + 2 * HT;                    // u^{k-1} row slot
+  static constexpr size_t smem_bytes =
+      size_t(NS) * RB * (LU + LK) * sizeof(T) + 2 * NS * sizeof(uint64_t) + 2 * NS * sizeof(int);
+  static_assert(WO > 0, "halo too wide for one warp");
+};
+
+template <typename T>
+__device__ __forceinline__ T shfl_up1(T x) {
+  return __shfl_up_sync(0xffffffffu, x, 1);
+}
+template <typename T>
+__device__ __forceinline__ T shfl_down1(T x) {
+  return __shfl_down_sync(0xffffffffu, x, 1);
+}
+
+template <typename T, int A, class S, int TS, int NW, int RB, int NS>
+__global__ void __launch_bounds__((NW + 1) * 32)
+    k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
+  constexpr int R = S::R;
+  using G = TBGeom<T, NW, RB, NS, R, TS>;
+  constexpr int V = G::V, HT = G::HT, WO = G::WO, W = G::W, LU = G::LU, LK = G::LK;
+  constexpr int WC = V + 2 * R;  // window row: R left | V own | R right
+  static_assert(R <= V, "neighbour vector must cover the radius");
+  using Ar = Arith<T, A>;
+  using acc_t = typename Ar::acc_t;
+  using coef_t = typename Ar::coef_t;
+  using vec_t = typename Vec<T>::type;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* s_uk = reinterpret_cast<T*>(smem_raw);
+  T* s_km = s_uk + NS * RB * LU;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_km + NS * RB * LK);
+  uint64_t* empty = full + NS;
+  int* s_tile = reinterpret_cast<int*>(empty + NS);
+  int* s_mlo = s_tile + NS;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const T* __restrict__ uk = static_cast<const T*>(p.uk);
+  const T* __restrict__ ukm1 = static_cast<const T*>(p.ukm1);
+  T* __restrict__ out_prev = static_cast<T*>(p.out_prev);
+  T* __restrict__ out_last = static_cast<T*>(p.out_last);
+  const int64_t pitch = p.pitch;
+  constexpr int NE_EXTRA = 2 * R * TS;  // u^k rows beyond the chunk (both sides)
+
+  if (warp == NW) {
+    if (lane == 0) {
+      const uint64_t pol_uk = l2_policy_evict_normal();
+      const uint64_t pol_km = l2_policy_evict_first();
+      uint32_t g = 0;
+      int tile = blockIdx.x;
+      while (tile < p.ntiles) {
+        const int chunk = tile / p.nstrips;
+        const int strip = tile - chunk * p.nstrips;
+        const int i0 = p.rlo + chunk * p.rc;
+        const int i1 = min(i0 + p.rc, p.rhi);
+        const int j0 = strip * W;
+        // columns: u^k from j0-HT-V, u^{k-1} from j0-HT; clamp to the allocation row
+        const int cu0 = j0 - HT - V, ck0 = j0 - HT;
+        const int nu = max(0, min(LU, p.cmax - cu0)) / V * V;
+        const int nk = max(0, min(LK, p.cmax - ck0)) / V * V;
+        const uint32_t ub = uint32_t(nu) * sizeof(T), kb = uint32_t(nk) * sizeof(T);
+        const int ne = (i1 - i0) + NE_EXTRA;
+        for (int mlo = 0; mlo < ne; mlo += RB, ++g) {
+          const uint32_t s = g % NS;
+          const uint32_t k = g / NS;
+          if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+          s_tile[s] = tile;
+          s_mlo[s] = mlo;
+          const int mhi = min(mlo + RB, ne);
+          uint32_t bytes = 0;
+          for (int m = mlo; m < mhi; ++m) {
+            const int e = i0 - R * TS + m;
+            if (e >= p.gmin && e < p.gmax) bytes += ub;
+            const int ek = e - R;
+            if (m >= 2 * R && ek >= p.gmin && ek < p.gmax) bytes += kb;
+          }
+          mbar_arrive_expect_tx(&full[s], bytes);
+          for (int m = mlo; m < mhi; ++m) {
+            const int e = i0 - R * TS + m;
+            if (e >= p.gmin && e < p.gmax && ub)
+              tma_load_1d(s_uk + (s * RB + (m - mlo)) * LU, uk + int64_t(e) * pitch + cu0, ub,
+                          &full[s], pol_uk);
+            const int ek = e - R;
+            if (m >= 2 * R && ek >= p.gmin && ek < p.gmax && kb)
+              tma_load_1d(s_km + (s * RB + (m - mlo)) * LK, ukm1 + int64_t(ek) * pitch + ck0, kb,
+                          &full[s], pol_km);
+          }
+        }
+        tile = int(gridDim.x + atomicAdd(&g_tile_next[slot], 1u));
+      }
+      const uint32_t s = g % NS;
+      const uint32_t k = g / NS;
+      if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+      s_tile[s] = -1;
+      mbar_arrive(&full[s]);
+      __threadfence();
+      if (atomicAdd(&g_tile_done[slot], 1u) == gridDim.x - 1) {
+        g_tile_next[slot] = 0;
+        g_tile_done[slot] = 0;
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ------------------------------------------------
+  coef_t c[S::N];
+#pragma unroll
+  for (int s = 0; s < S::N; ++s) {
+    if constexpr (sizeof(coef_t) == sizeof(double))
+      c[s] = p.c[s];
+    else
+      c[s] = p.cf[s];
+  }
+  // win[t] holds level k+t rows (oldest first), t = 0..TS-1
+  T win[TS][2 * R + 1][WC];
+#pragma unroll
+  for (int t = 0; t < TS; ++t)
+#pragma unroll
+    for (int r = 0; r < 2 * R + 1; ++r)
+#pragma unroll
+      for (int x = 0; x < WC; ++x) win[t][r][x] = T(0);
+
+  const int xo = V + warp * WO + lane * V;  // own vector's column in the u^k slot
+  const int xk = warp * WO + lane * V;      // own vector's column in the u^{k-1} slot
+  const bool lane_out = (lane * V >= HT) && (lane * V + V <= HT + WO);
+
+  auto stage_out = [&](int t, const T* minus, int row, int gc0, T* res) {
+    // level k+t+1 at `row` from window t; minus = level k+t-1 at the same row
+    const int gi = p.row0 + row;
+    const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      acc_t a = Ar::zero();
+#pragma unroll
+      for (int s = 0; s < S::N; ++s)
+        a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
+      const int gc = gc0 + v;
+      const bool in = row_in && (gc >= p.ring) && (gc < p.cols - p.ring);
+      res[v] = in ? Ar::two(a, minus[v]) : T(0);
+    }
+  };
+
+  auto admit = [&](int t, const T* own) {
+    // slide window t and admit a new row whose own vector is `own`; neighbours by shuffle
+#pragma unroll
+    for (int r = 0; r < 2 * R; ++r)
+#pragma unroll
+      for (int x = 0; x < WC; ++x) win[t][r][x] = win[t][r + 1][x];
+#pragma unroll
+    for (int v = 0; v < V; ++v) win[t][2 * R][R + v] = own[v];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      win[t][2 * R][q] = shfl_up1(own[V - R + q]);   // left neighbour's last R values
+      win[t][2 * R][R + V + q] = shfl_down1(own[q]);  // right neighbour's first R values
+    }
+  };
+
+  auto row_step = [&](const T* su_row, const T* sk_row, int m, int i0, int i1, int j0) {
+    // ---- admit u^k row e = i0 - R*TS + m into window 0 from shared memory
+#pragma unroll
+    for (int r = 0; r < 2 * R; ++r)
+#pragma unroll
+      for (int x = 0; x < WC; ++x) win[0][r][x] = win[0][r + 1][x];
+    {
+      T l[V], o[V], rr[V];
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - V), l);
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo), o);
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + V), rr);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        win[0][2 * R][q] = l[V - R + q];
+        win[0][2 * R][R + V + q] = rr[q];
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) win[0][2 * R][R + v] = o[v];
+    }
+    const int e = i0 - R * TS + m;
+    const int gc0 = j0 - HT + warp * WO + lane * V;
+    // ---- stages: stage t+1 produces level k+t+1 at row e - (t+1)R once window t is full
+#pragma unroll
+    for (int t = 0; t < TS; ++t) {
+      if (m < 2 * R * (t + 1)) break;
+      const int row = e - (t + 1) * R;
+      T minus[V];
+      if (t == 0) {
+        Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + xk), minus);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) minus[v] = win[t - 1][0][R + v];
+      }
+      T res[V];
+      stage_out(t, minus, row, gc0, res);
+      const bool store_row = row >= i0 && row < i1 && lane_out && gc0 < p.cols;
+      if (t == TS - 1) {
+        if (store_row) {
+          T* dst = out_last + int64_t(row) * pitch + gc0;
+          if (gc0 + V <= p.cols) {
+            *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+              if (gc0 + v < p.cols) dst[v] = res[v];
+          }
+        }
+      } else {
+        if (t == TS - 2 && store_row) {
+          T* dst = out_prev + int64_t(row) * pitch + gc0;
+          if (gc0 + V <= p.cols) {
+            *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
+          } else {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+              if (gc0 + v < p.cols) dst[v] = res[v];
+          }
+        }
+        admit(t + 1, res);
+      }
+    }
+  };
+
+  for (uint32_t g = 0;; ++g) {
+    const uint32_t s = g % NS;
+    const uint32_t k = g / NS;
+    mbar_wait(&full[s], k & 1);
+    const int tile = s_tile[s];
+    if (tile < 0) break;
+    const int mlo = s_mlo[s];
+    const int chunk = tile / p.nstrips;
+    const int strip = tile - chunk * p.nstrips;
+    const int i0 = p.rlo + chunk * p.rc;
+    const int i1 = min(i0 + p.rc, p.rhi);
+    const int j0 = strip * W;
+    const int ne = (i1 - i0) + NE_EXTRA;
+    const T* su = s_uk + s * RB * LU;
+    const T* sk = s_km + s * RB * LK;
+    if (mlo + RB <= ne) {
+#pragma unroll
+      for (int mm = 0; mm < RB; ++mm) row_step(su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0);
+    } else {
+      for (int mm = 0; mm < ne - mlo; ++mm)
+        row_step(su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+

@@ -34,7 +34,7 @@ class Simulation:
     (default: the scheme radius); periodic grids hold n^2 independent nodes."""
 
     def __init__(self, scheme, n: int, lam: float, bc: str = "dirichlet", ring: int | None = None,
-                 dtype: str = "f64", arith: str = "ref", c: float = 1.0):
+                 dtype: str = "f64", arith: str = "ref", c: float = 1.0, tsteps: int = 1):
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         if bc not in nat.BC:
             raise ValueError(f"bc must be one of {tuple(nat.BC)}, got {bc!r}")
@@ -46,7 +46,14 @@ class Simulation:
         self.ring = (radius if ring is None else int(ring)) if bc == "dirichlet" else 0
         self.rows = self.n + 1 if bc == "dirichlet" else self.n
         self.grid = nat.make_grid(self.rows, self.rows, max(2, radius), self.ring, bc, dtype, arith)
-        self.levels = [nat.Level(self.grid) for _ in range(3)]
+        if tsteps not in (1, 2, 4):
+            raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
+        if tsteps > 1 and bc != "dirichlet":
+            raise ValueError("temporal blocking supports Dirichlet grids only")
+        self.tsteps = int(tsteps)
+        # temporal blocking writes two new levels while both inputs are still read: 4 levels
+        self.levels = [nat.Level(self.grid) for _ in range(3 if tsteps == 1 else 4)]
+        self.previous = None
         self.t_first_u = nat.make_table(evaluate_table(self.spec.first_u, self.lam))
         self.t_first_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
         self.t_two = nat.make_table(evaluate_table(self.spec.two_step, self.lam))
@@ -112,19 +119,25 @@ class Simulation:
         """u^1 from (u^0 = levels[1], v0 = levels[0]) into levels[2]."""
         nat.first_step(self.grid, self.levels[1], self.levels[0], self.levels[2], self.t_first_u,
                        self.t_first_v, self.tau, stream)
-        self.newest, self.step = 2, 1
+        self.newest, self.previous, self.step = 2, 1, 1
 
     def march(self, nsteps: int, stream=None):
         """``nsteps`` two-step updates, rotating the three levels in place."""
         if self.newest is None:
             raise RuntimeError("call first_step() before march()")
-        self.newest = nat.march(self.grid, self.levels, nsteps, self.t_two, self.newest, stream)
+        if self.tsteps == 1:
+            self.newest = nat.march(self.grid, self.levels, nsteps, self.t_two, self.newest, stream)
+            self.previous = (self.newest + 2) % 3
+        else:
+            self.newest, self.previous = nat.march_tb(self.grid, self.levels, nsteps, self.t_two,
+                                                      self.tsteps, self.newest, self.previous,
+                                                      stream)
         self.step += int(nsteps)
 
     # ---- read-back ----------------------------------------------------------------
     def field(self, which: str = "newest") -> np.ndarray:
         """Latest (or previous) level as the reference's (n+1)^2 array."""
-        idx = self.newest if which == "newest" else (self.newest + 2) % 3
+        idx = self.newest if which == "newest" else self.previous
         return self.levels[idx].download(self.n + 1, self.n + 1)
 
     def initial_fields(self):

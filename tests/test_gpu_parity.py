@@ -323,3 +323,47 @@ def test_config4_full_size_slab_check(oracle):
     # the band's first/last columns are the global ring (zero in both)
     assert same_bits(got, want)
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------ temporal blocking (K3)
+@pytest.mark.parametrize("name,radius", SHAPES)
+@pytest.mark.parametrize("dtype,arith", [("f64", "ref"), ("f32", "ref"), ("f32", "native")])
+@pytest.mark.parametrize("tsteps", [2, 4])
+@pytest.mark.parametrize("n", [45, 700])
+def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps, n, oracle):
+    """T fused steps per pass equal T single steps bit for bit (incl. a remainder step)."""
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation(name, n, 0.4 if radius == 2 else 0.6, bc="dirichlet", dtype=dtype,
+                     arith=arith, tsteps=tsteps)
+    rng = np.random.default_rng(7 * n + tsteps)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    v0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    sim.load_initial(u0, v0)
+    sim.first_step()
+    steps = 2 * tsteps + 1
+    sim.march(steps)
+    o1 = oracle.first_step(u0, v0, pairs(sim.spec, "first_u", sim.lam),
+                           pairs(sim.spec, "first_v", sim.lam), sim.tau, "dirichlet", radius, arith)
+    want, want_prev = oracle.march(o1, u0, pairs(sim.spec, "two_step", sim.lam), steps,
+                                   "dirichlet", radius, arith)
+    assert same_bits(sim.field(), want)
+    assert same_bits(sim.field("previous"), want_prev)
+
+
+def test_temporal_blocking_large_grid_matches_single_steps():
+    """C5 shape (P13, ring 2, f32 native) on a 4096^2 grid: T=2 and T=4 marches equal the
+    T=1 march bit for bit after 12 steps."""
+    from paper_1904_04048_b200.device import Simulation
+
+    res = {}
+    for ts in (1, 2, 4):
+        sim = Simulation("P13", 4095, 0.4, bc="dirichlet", dtype="f32", arith="native", tsteps=ts)
+        sim.gaussian_initial(16, 0.002, 0.01, seed=0)
+        sim.first_step()
+        sim.march(12)
+        res[ts] = (sim.field(), sim.field("previous"))
+    for ts in (2, 4):
+        assert same_bits(res[ts][0], res[1][0]), ts
+        assert same_bits(res[ts][1], res[1][1]), ts
