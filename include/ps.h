@@ -169,6 +169,20 @@ ps_status ps_gaussian_sum(const ps_grid* g, void* level, int32_t K, const double
                           const double* cy, const double* width, const double* amp,
                           int64_t n, void* stream);
 
+/* Fused per-step error sums of run() for the standing-wave benchmark (
+ * replaces simulator.py:275-280 when `exact` is the default standing wave):
+ *   ref = S * st;  out2[0] = sum((u - ref)^2);  out2[1] = sum(ref^2)
+ * over the rows_h x cols_h block from logical (0,0) (the reference's (n+1)^2 array incl.
+ * ring / alias), summed in numpy's pairwise order so both floats equal the reference's
+ * bit for bit.  S (same layout as the level) holds sin(2πx1)*sin(2πx2) as numpy computes
+ * it; st = sin(2√2 π c t).  out2 is a DEVICE pointer.  f64 grids only.
+ * ps_errsum_create allocates the per-size summation plan (not a hot call). */
+typedef struct ps_errsum ps_errsum;
+ps_errsum* ps_errsum_create(int64_t rows_h, int64_t cols_h);
+ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, const void* S,
+                         double st, double* out2, void* stream);
+void ps_errsum_destroy(ps_errsum* e);
+
 /* Kernel launches issued by this library since load (for launch accounting). */
 int64_t ps_launch_count(void);
 

@@ -51,7 +51,8 @@ class PsTable(ctypes.Structure):
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
            "ps_march", "ps_two_step_tb", "ps_march_tb",
-           "ps_gaussian_sum", "ps_launch_count", "ps_strerror", "ps_version")
+           "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
+           "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -86,6 +87,9 @@ def load_library(path: str = LIB_PATH):
             "ps_march_tb": (i32, [G, ctypes.POINTER(vp), i64, T, i32, ctypes.POINTER(i32),
                                   ctypes.POINTER(i32), vp]),
             "ps_gaussian_sum": (i32, [G, vp, i32, vp, vp, vp, vp, i64, vp]),
+            "ps_errsum_create": (vp, [i64, i64]),
+            "ps_errsum_step": (i32, [vp, G, vp, vp, dbl, vp, vp]),
+            "ps_errsum_destroy": (None, [vp]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
             "ps_version": (ctypes.c_char_p, []),
@@ -251,6 +255,30 @@ def gaussian_sum(grid, level: Level, centres, widths, amps, n: int, stream=None)
     check(load_library().ps_gaussian_sum(ctypes.byref(grid), level.ptr, len(a), p(cx), p(cy),
                                          p(w), p(a), int(n), stream or current_stream()),
           "ps_gaussian_sum")
+
+
+class ErrSum:
+    """Device plan for run()'s per-step error sums in numpy's pairwise order (F1)."""
+
+    def __init__(self, rows_h: int, cols_h: int):
+        _torch()
+        self._lib = load_library()
+        self.handle = self._lib.ps_errsum_create(int(rows_h), int(cols_h))
+        if not self.handle:
+            raise PsStatusError(5, "ps_errsum_create")
+
+    def step(self, grid, level: Level, S: Level, st: float, out_ptr: int, stream=None):
+        check(self._lib.ps_errsum_step(ctypes.c_void_p(self.handle), ctypes.byref(grid),
+                                       level.ptr, S.ptr, float(st), ctypes.c_void_p(out_ptr),
+                                       stream or current_stream()), "ps_errsum_step")
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h:
+            try:
+                self._lib.ps_errsum_destroy(ctypes.c_void_p(h))
+            except Exception:
+                pass
 
 
 def launch_count() -> int:

@@ -19,6 +19,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "ps.h"
 #include "ps_arith.cuh"
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
 }
 
 #include "ps_tblock.cuh"
+#include "ps_errsum.cuh"
 
 // ---------------------------------------------------------------------------
 // Generic kernels (any tap list within the ghost width; first step; images)
@@ -715,7 +719,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 #define PS_TB_NW 4
 #endif
 #ifndef PS_TB_RB
-#define PS_TB_RB 4
+#define PS_TB_RB 0  // 0: 2R+1 rows per stage, so a stage is one full window rotation
 #endif
 #ifndef PS_TB_NS
 #define PS_TB_NS 4
@@ -725,7 +729,8 @@ template <typename T, int A, class S, int TS>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st) {
-  constexpr int NW = PS_TB_NW, RB = PS_TB_RB, NS = PS_TB_NS;
+  constexpr int NW = PS_TB_NW, NS = PS_TB_NS;
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
   auto kern = k_two_step_tb<T, A, S, TS, NW, RB, NS>;
   static std::once_flag once;
@@ -1184,6 +1189,153 @@ ps_status ps_gaussian_sum(const ps_grid* g, void* level, int32_t K, const double
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if ((s = last_cuda_status()) != PS_OK) return s;
   return ps_fill_ghosts(g, level, 0, stream);
+}
+
+struct ps_errsum {
+  ps::ErrsumPlan plan;
+};
+
+ps_errsum* ps_errsum_create(int64_t rows_h, int64_t cols_h) {
+  if (rows_h < 1 || cols_h < 1) return nullptr;
+  const int64_t N = rows_h * cols_h;
+  struct Ref {
+    bool leaf;
+    int32_t idx;
+  };
+  struct Internal {
+    Ref l, r;
+    int32_t height;
+  };
+  std::vector<int64_t> ls;
+  std::vector<int32_t> ll;
+  std::vector<Internal> ints;
+  // numpy's pairwise order: ranges <= 128 are leaves, larger ones split at n/2 rounded
+  // down to a multiple of 8 (explicit stack instead of recursion).
+  struct Frame {
+    int64_t start, n;
+    int state;
+    Ref left;
+    int32_t hl;
+  };
+  std::vector<Frame> stack;
+  stack.push_back({0, N, 0, {true, 0}, 0});
+  Ref ret{true, 0};
+  int32_t ret_h = 0;
+  while (!stack.empty()) {
+    Frame& f = stack.back();
+    if (f.n <= ps::kPwBlock) {
+      ls.push_back(f.start);
+      ll.push_back(int32_t(f.n));
+      ret = {true, int32_t(ls.size() - 1)};
+      ret_h = 0;
+      stack.pop_back();
+      continue;
+    }
+    int64_t n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      const int64_t st0 = f.start;
+      stack.push_back({st0, n2, 0, {true, 0}, 0});
+    } else if (f.state == 1) {
+      f.state = 2;
+      f.left = ret;
+      f.hl = ret_h;
+      const int64_t st1 = f.start + n2, n1 = f.n - n2;
+      stack.push_back({st1, n1, 0, {true, 0}, 0});
+    } else {
+      const int32_t h = std::max(f.hl, ret_h) + 1;
+      ints.push_back({f.left, ret, h});
+      ret = {false, int32_t(ints.size() - 1)};
+      ret_h = h;
+      stack.pop_back();
+    }
+  }
+  const int32_t L = int32_t(ls.size()), I = int32_t(ints.size());
+  auto id_of = [&](const Ref& r) { return r.leaf ? r.idx : L + r.idx; };
+  int32_t H = 0;
+  for (const auto& in : ints) H = std::max(H, in.height);
+  std::vector<int32_t> nid, nl, nr, off(size_t(H) + 1, 0);
+  for (int32_t h = 1; h <= H; ++h) {
+    off[size_t(h - 1)] = int32_t(nid.size());
+    for (int32_t k = 0; k < I; ++k)
+      if (ints[size_t(k)].height == h) {
+        nid.push_back(L + k);
+        nl.push_back(id_of(ints[size_t(k)].l));
+        nr.push_back(id_of(ints[size_t(k)].r));
+      }
+  }
+  off[size_t(H)] = int32_t(nid.size());
+  auto* e = new ps_errsum;
+  ps::ErrsumPlan& p = e->plan;
+  p.rows_h = rows_h;
+  p.cols_h = cols_h;
+  p.count = N;
+  p.nleaves = L;
+  p.ninternal = I;
+  p.nlevels = H;
+  p.root = id_of(ret);
+  p.h_level_off = off;
+  bool ok = cudaMalloc(&p.leaf_start, sizeof(int64_t) * size_t(L)) == cudaSuccess &&
+            cudaMalloc(&p.leaf_len, sizeof(int32_t) * size_t(L)) == cudaSuccess &&
+            cudaMalloc(&p.node_left, sizeof(int32_t) * (size_t(I) + 1)) == cudaSuccess &&
+            cudaMalloc(&p.node_right, sizeof(int32_t) * (size_t(I) + 1)) == cudaSuccess &&
+            cudaMalloc(&p.node_id, sizeof(int32_t) * (size_t(I) + 1)) == cudaSuccess &&
+            cudaMalloc(&p.level_off, sizeof(int32_t) * (size_t(H) + 1)) == cudaSuccess &&
+            cudaMalloc(&p.values, sizeof(double) * 2 * size_t(L + I)) == cudaSuccess;
+  ok = ok && cudaMemcpy(p.leaf_start, ls.data(), sizeof(int64_t) * size_t(L),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+  ok = ok && cudaMemcpy(p.leaf_len, ll.data(), sizeof(int32_t) * size_t(L),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+  if (I > 0) {
+    ok = ok && cudaMemcpy(p.node_left, nl.data(), sizeof(int32_t) * size_t(I),
+                          cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(p.node_right, nr.data(), sizeof(int32_t) * size_t(I),
+                          cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && cudaMemcpy(p.node_id, nid.data(), sizeof(int32_t) * size_t(I),
+                          cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  ok = ok && cudaMemcpy(p.level_off, off.data(), sizeof(int32_t) * (size_t(H) + 1),
+                        cudaMemcpyHostToDevice) == cudaSuccess;
+  if (!ok) {
+    ps_errsum_destroy(e);
+    return nullptr;
+  }
+  return e;
+}
+
+void ps_errsum_destroy(ps_errsum* e) {
+  if (!e) return;
+  ps::ErrsumPlan& p = e->plan;
+  cudaFree(p.leaf_start);
+  cudaFree(p.leaf_len);
+  cudaFree(p.node_left);
+  cudaFree(p.node_right);
+  cudaFree(p.node_id);
+  cudaFree(p.level_off);
+  cudaFree(p.values);
+  delete e;
+}
+
+ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, const void* S,
+                         double st, double* out2, void* stream) {
+  if (!e) return PS_ERR_ARG;
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!level || !S || !out2) return PS_ERR_ARG;
+  if (g->dtype != PS_F64) return PS_ERR_ARG;
+  const ps::ErrsumPlan& p = e->plan;
+  const int64_t extra = g->bc == PS_BC_PERIODIC ? g->ghost : 0;
+  if (p.rows_h > g->rows + extra || p.cols_h > g->cols + extra) return PS_ERR_SHAPE;
+  cudaStream_t st_ = static_cast<cudaStream_t>(stream);
+  const int32_t nvalues = p.nleaves + p.ninternal;
+  k_errsum_leaves<<<unsigned((p.nleaves + 127) / 128), 128, 0, st_>>>(
+      at_origin<double>(g, level), at_origin<double>(g, S), g->pitch, p.cols_h, st,
+      p.leaf_start, p.leaf_len, p.nleaves, p.values, nvalues);
+  k_errsum_fold<<<1, 1024, 0, st_>>>(p.node_left, p.node_right, p.node_id, p.level_off,
+                                      p.nlevels, p.values, nvalues, p.root, out2);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  return last_cuda_status();
 }
 
 int64_t ps_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

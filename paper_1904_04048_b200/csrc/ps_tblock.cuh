@@ -181,19 +181,31 @@ __global__ void __launch_bounds__((NW + 1) * 32)
   const int xk = warp * WO + lane * V;      // own vector's column in the u^{k-1} slot
   const bool lane_out = (lane * V >= HT) && (lane * V + V <= HT + WO);
 
-  auto stage_out = [&](int t, const T* minus, int row, int gc0, T* res) {
+  const int gc_lane = warp * WO + lane * V - HT;  // own column relative to the strip start
+
+  auto stage_out = [&](int t, const T* minus, int row, int gc0, bool cols_inner, T* res) {
     // level k+t+1 at `row` from window t; minus = level k+t-1 at the same row
-    const int gi = p.row0 + row;
-    const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
+    acc_t acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       acc_t a = Ar::zero();
 #pragma unroll
       for (int s = 0; s < S::N; ++s)
         a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
-      const int gc = gc0 + v;
-      const bool in = row_in && (gc >= p.ring) && (gc < p.cols - p.ring);
-      res[v] = in ? Ar::two(a, minus[v]) : T(0);
+      acc[v] = a;
+    }
+    const int gi = p.row0 + row;
+    const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
+    if (row_in && cols_inner) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) res[v] = Ar::two(acc[v], minus[v]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int gc = gc0 + v;
+        const bool in = row_in && (gc >= p.ring) && (gc < p.cols - p.ring);
+        res[v] = in ? Ar::two(acc[v], minus[v]) : T(0);
+      }
     }
   };
 
@@ -212,31 +224,47 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     }
   };
 
-  auto row_step = [&](const T* su_row, const T* sk_row, int m, int i0, int i1, int j0) {
-    // ---- admit u^k row e = i0 - R*TS + m into window 0 from shared memory
+  auto admit_uk = [&](const T* su_row) {
 #pragma unroll
     for (int r = 0; r < 2 * R; ++r)
 #pragma unroll
       for (int x = 0; x < WC; ++x) win[0][r][x] = win[0][r + 1][x];
-    {
-      T l[V], o[V], rr[V];
-      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - V), l);
-      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo), o);
-      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + V), rr);
+    T l[V], o[V], rr[V];
+    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - V), l);
+    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo), o);
+    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + V), rr);
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        win[0][2 * R][q] = l[V - R + q];
-        win[0][2 * R][R + V + q] = rr[q];
-      }
-#pragma unroll
-      for (int v = 0; v < V; ++v) win[0][2 * R][R + v] = o[v];
+    for (int q = 0; q < R; ++q) {
+      win[0][2 * R][q] = l[V - R + q];
+      win[0][2 * R][R + V + q] = rr[q];
     }
+#pragma unroll
+    for (int v = 0; v < V; ++v) win[0][2 * R][R + v] = o[v];
+  };
+
+  auto store_vec = [&](T* base, int row, int gc0, const T* res) {
+    T* dst = base + int64_t(row) * pitch + gc0;
+    if (gc0 + V <= p.cols) {
+      *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+        if (gc0 + v < p.cols) dst[v] = res[v];
+    }
+  };
+
+  // One u^k row through every stage.  STEADY: all TS windows are full and the final row
+  // lies inside the tile (no per-stage checks, so the unrolled window rotation compiles
+  // to register renaming).  Otherwise stage t+1 runs only once window t is full.
+  auto row_step = [&](auto steady_tag, const T* su_row, const T* sk_row, int m, int i0, int i1,
+                      int j0, bool cols_inner, bool lane_store) {
+    constexpr bool STEADY = decltype(steady_tag)::value;
+    admit_uk(su_row);
     const int e = i0 - R * TS + m;
-    const int gc0 = j0 - HT + warp * WO + lane * V;
-    // ---- stages: stage t+1 produces level k+t+1 at row e - (t+1)R once window t is full
+    const int gc0 = j0 + gc_lane;
 #pragma unroll
     for (int t = 0; t < TS; ++t) {
-      if (m < 2 * R * (t + 1)) break;
+      if (!STEADY && m < 2 * R * (t + 1)) break;
       const int row = e - (t + 1) * R;
       T minus[V];
       if (t == 0) {
@@ -246,30 +274,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         for (int v = 0; v < V; ++v) minus[v] = win[t - 1][0][R + v];
       }
       T res[V];
-      stage_out(t, minus, row, gc0, res);
-      const bool store_row = row >= i0 && row < i1 && lane_out && gc0 < p.cols;
+      stage_out(t, minus, row, gc0, cols_inner, res);
       if (t == TS - 1) {
-        if (store_row) {
-          T* dst = out_last + int64_t(row) * pitch + gc0;
-          if (gc0 + V <= p.cols) {
-            *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
-          } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-              if (gc0 + v < p.cols) dst[v] = res[v];
-          }
-        }
+        if (lane_store && (STEADY || (row >= i0 && row < i1))) store_vec(out_last, row, gc0, res);
       } else {
-        if (t == TS - 2 && store_row) {
-          T* dst = out_prev + int64_t(row) * pitch + gc0;
-          if (gc0 + V <= p.cols) {
-            *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
-          } else {
-#pragma unroll
-            for (int v = 0; v < V; ++v)
-              if (gc0 + v < p.cols) dst[v] = res[v];
-          }
-        }
+        if (t == TS - 2 && lane_store && row >= i0 && row < i1)
+          store_vec(out_prev, row, gc0, res);
         admit(t + 1, res);
       }
     }
@@ -290,12 +300,19 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     const int ne = (i1 - i0) + NE_EXTRA;
     const T* su = s_uk + s * RB * LU;
     const T* sk = s_km + s * RB * LK;
-    if (mlo + RB <= ne) {
+    // whole strip away from the global ring and the right edge: no column masks
+    const bool cols_inner = (j0 - HT >= p.ring) && (j0 + W + HT <= p.cols - p.ring);
+    const bool lane_store = lane_out && (j0 + gc_lane < p.cols);
+    if (mlo >= 2 * R * TS && mlo + RB <= ne) {
 #pragma unroll
-      for (int mm = 0; mm < RB; ++mm) row_step(su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0);
+      for (int mm = 0; mm < RB; ++mm)
+        row_step(std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner,
+                 lane_store);
     } else {
-      for (int mm = 0; mm < ne - mlo; ++mm)
-        row_step(su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0);
+#pragma unroll 1
+      for (int mm = 0; mm < min(RB, ne - mlo); ++mm)
+        row_step(std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner,
+                 lane_store);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
