@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 NVFLAGS = -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo \
           -Xcompiler -fPIC -Xcompiler -Wall -shared -Iinclude
 SRC = paper_1904_04048_b200/csrc/ps_device.cu
-HDR = include/ps.h paper_1904_04048_b200/csrc/ps_arith.cuh paper_1904_04048_b200/csrc/ps_ptx.cuh
+HDR = include/ps.h $(wildcard paper_1904_04048_b200/csrc/*.cuh)
 
 all: paper_1904_04048_b200/libps.so oracle
 

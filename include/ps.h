@@ -50,9 +50,10 @@ typedef enum ps_dtype { PS_F64 = 0, PS_F32 = 1 } ps_dtype;
  *   PS_ARITH_REF    — the reference's own operation sequence, bit for bit (simulator.py:147-191):
  *                     f64: acc = +0.0; acc = fl(acc + fl(c*u)) in table order, no FMA;
  *                     f32: products in f32, accumulation in f64, cast to f32, f32 subtract.
- *   PS_ARITH_NATIVE — f32 only: the same ordered, FMA-free sequence carried out entirely in
- *                     f32 (no f64 accumulator).  Compared against the f64 oracle within a
- *                     stated tolerance.  For f64 it is identical to PS_ARITH_REF. */
+ *   PS_ARITH_NATIVE — f32 only: taps in the same table order folded with one correctly
+ *                     rounded fma each (acc = fma(c, u, acc) from +0.0, f32 accumulator),
+ *                     then an f32 subtract.  Bitwise against the oracle's fmaf() chain;
+ *                     against the f64 run within a stated tolerance.  f64: same as REF. */
 typedef enum ps_arith { PS_ARITH_REF = 0, PS_ARITH_NATIVE = 1 } ps_arith;
 
 #define PS_MAX_TAPS 32
@@ -135,6 +136,25 @@ ps_status ps_two_step(const ps_grid* g, const void* uk, const void* ukm1, void* 
  * concurrently. */
 ps_status ps_two_step_rows(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
                            const ps_table* t, int64_t row_lo, int64_t row_hi, void* stream);
+
+/* Row-slab update with in-kernel halo delivery (the fused variant):
+ * as ps_two_step_rows, and the CTAs that write the first / last R rows also store them
+ * straight into the neighbour slabs' ghost rows — `up_ukp1` (the u^{k+1} level of the
+ * slab above, whose logical rows number `up_rows`) receives rows [0,R) at its rows
+ * [up_rows, up_rows+R); `dn_ukp1` (slab below) receives rows [rows-R, rows) at its rows
+ * [-R, 0).  Peer pointers are allocation bases (as from ps_ipc_open) on any device
+ * reachable by peer access (NVLink); NULL = no neighbour.  Dirichlet slabs only.  The
+ * caller orders the next step after the neighbours' launches (event / NCCL token). */
+ps_status ps_two_step_halo(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                           const ps_table* t, int64_t row_lo, int64_t row_hi, void* up_ukp1,
+                           int64_t up_rows, void* dn_ukp1, void* stream);
+
+/* CUDA IPC plumbing for peer levels across processes (64-byte opaque handles).
+ * ps_ipc_get_handle names the allocation containing dev_ptr and returns dev_ptr's byte
+ * offset in it; the receiver adds that offset to the pointer ps_ipc_open returns. */
+ps_status ps_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset);
+ps_status ps_ipc_open(const void* handle64, void** dev_ptr);
+ps_status ps_ipc_close(void* dev_ptr);
 
 /* nsteps two-step updates rotating three levels in place (the loop of run(),
  * simulator.py:271-274).  On entry lvl[*newest] = u^k and lvl[(*newest+2)%3] = u^{k-1};

@@ -15,8 +15,9 @@
  * Per point: acc = +0.0; for each tap in table order acc = fl(acc + fl(c * u[nb]));
  * no FMA (built with -ffp-contract=off).  float32 fields follow numpy's promotion:
  * fl32(fl32(c) * u) added into a float64 accumulator, stored to float32, float32
- * subtract / add (simulator.py:150-154, 179, 184).  The "native" f32 contract keeps
- * the accumulator in float32 (the GPU's PS_ARITH_NATIVE).
+ * subtract / add (simulator.py:150-154, 179, 184).  The "native" f32 contract is the
+ * GPU's own (PS_ARITH_NATIVE, not a reference path): taps folded in with fmaf() in
+ * table order, float32 accumulator.
  *
  * Generalisation beyond the reference: the Dirichlet ring width is
  * a parameter (reference: 1, simulator.py:98-102); at ring = 1 the arithmetic is the
@@ -27,6 +28,7 @@
  */
 #include <stdint.h>
 #include <stdlib.h>
+#include <math.h>
 #include <string.h>
 #ifdef _OPENMP
 #include <omp.h>
@@ -87,6 +89,8 @@ static void row_acc_f32ref(const tab_t* t, const float* u, int64_t cols, int per
   }
 }
 
+/* GPU "native" f32 contract (not a reference path): acc = fmaf(c, u, acc) per tap in
+ * table order from +0.0 — one correctly rounded fused multiply-add per tap. */
 static void row_acc_f32nat(const tab_t* t, const float* u, int64_t cols, int per, int64_t n1,
                            int64_t n2, int64_t i, int64_t j0, int64_t j1, float* acc) {
   for (int64_t j = j0; j < j1; ++j) acc[j - j0] = 0.0f;
@@ -94,10 +98,11 @@ static void row_acc_f32nat(const tab_t* t, const float* u, int64_t cols, int per
     const float c = (float)t->c[s];
     if (per) {
       const float* row = u + wrap(i + t->q1[s], n1) * cols;
-      for (int64_t j = j0; j < j1; ++j) acc[j - j0] = acc[j - j0] + c * row[wrap(j + t->q2[s], n2)];
+      for (int64_t j = j0; j < j1; ++j)
+        acc[j - j0] = fmaf(c, row[wrap(j + t->q2[s], n2)], acc[j - j0]);
     } else {
       const float* row = u + (i + t->q1[s]) * cols + t->q2[s];
-      for (int64_t j = j0; j < j1; ++j) acc[j - j0] = acc[j - j0] + c * row[j];
+      for (int64_t j = j0; j < j1; ++j) acc[j - j0] = fmaf(c, row[j], acc[j - j0]);
     }
   }
 }
@@ -248,7 +253,7 @@ int ora_first_step(int dtype, int arith, int bc, int ring, int64_t rows, int64_t
         if (arith == ORA_NATIVE) {
           row_acc_f32nat(&tu, (const float*)u0, cols, per, n1, n2, ic, jlo, jhi, fu);
           row_acc_f32nat(&tv, (const float*)v0, cols, per, n1, n2, ic, jlo, jhi, fv);
-          for (int64_t j = jlo; j < jhi; ++j) o[j] = fu[j - jlo] + tauf * fv[j - jlo];
+          for (int64_t j = jlo; j < jhi; ++j) o[j] = fmaf(tauf, fv[j - jlo], fu[j - jlo]);
         } else {
           row_acc_f32ref(&tu, (const float*)u0, cols, per, n1, n2, ic, jlo, jhi, au);
           row_acc_f32ref(&tv, (const float*)v0, cols, per, n1, n2, ic, jlo, jhi, av);

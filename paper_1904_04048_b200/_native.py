@@ -50,7 +50,8 @@ class PsTable(ctypes.Structure):
 
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
-           "ps_march", "ps_two_step_tb", "ps_march_tb",
+           "ps_march", "ps_two_step_tb", "ps_march_tb", "ps_two_step_halo", "ps_ipc_get_handle",
+           "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
            "ps_launch_count", "ps_strerror", "ps_version")
 
@@ -84,6 +85,10 @@ def load_library(path: str = LIB_PATH):
             "ps_two_step_rows": (i32, [G, vp, vp, vp, T, i64, i64, vp]),
             "ps_march": (i32, [G, ctypes.POINTER(vp), i64, T, ctypes.POINTER(i32), vp]),
             "ps_two_step_tb": (i32, [G, vp, vp, vp, vp, T, i32, vp]),
+            "ps_two_step_halo": (i32, [G, vp, vp, vp, T, i64, i64, vp, i64, vp, vp]),
+            "ps_ipc_get_handle": (i32, [vp, vp, ctypes.POINTER(i64)]),
+            "ps_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
+            "ps_ipc_close": (i32, [vp]),
             "ps_march_tb": (i32, [G, ctypes.POINTER(vp), i64, T, i32, ctypes.POINTER(i32),
                                   ctypes.POINTER(i32), vp]),
             "ps_gaussian_sum": (i32, [G, vp, i32, vp, vp, vp, vp, i64, vp]),
@@ -219,6 +224,37 @@ def two_step_rows(grid, uk: Level, ukm1: Level, out: Level, t: PsTable, lo: int,
     check(load_library().ps_two_step_rows(ctypes.byref(grid), uk.ptr, ukm1.ptr, out.ptr,
                                           ctypes.byref(t), int(lo), int(hi),
                                           stream or current_stream()), "ps_two_step_rows")
+
+
+def two_step_halo(grid, uk: Level, ukm1: Level, out: Level, t: PsTable, lo: int, hi: int,
+                  up_ptr: int | None, up_rows: int, dn_ptr: int | None, stream=None):
+    """Slab update that also stores its first/last R rows into the neighbours' ghost rows
+    (``up_ptr`` / ``dn_ptr``: allocation base pointers of their u^{k+1} levels)."""
+    check(load_library().ps_two_step_halo(ctypes.byref(grid), uk.ptr, ukm1.ptr, out.ptr,
+                                          ctypes.byref(t), int(lo), int(hi),
+                                          ctypes.c_void_p(up_ptr or 0), int(up_rows),
+                                          ctypes.c_void_p(dn_ptr or 0),
+                                          stream or current_stream()), "ps_two_step_halo")
+
+
+def ipc_handle(ptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding ``ptr``, byte offset of ptr)."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    check(load_library().ps_ipc_get_handle(ctypes.c_void_p(ptr), buf, ctypes.byref(off)),
+          "ps_ipc_get_handle")
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    out = ctypes.c_void_p(0)
+    check(load_library().ps_ipc_open(ctypes.create_string_buffer(handle, 64), ctypes.byref(out)),
+          "ps_ipc_open")
+    return out.value
+
+
+def ipc_close(ptr: int):
+    check(load_library().ps_ipc_close(ctypes.c_void_p(ptr)), "ps_ipc_close")
 
 
 def march(grid, levels, nsteps: int, t: PsTable, newest: int, stream=None) -> int:

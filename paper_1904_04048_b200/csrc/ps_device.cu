@@ -11,6 +11,7 @@
 //   * results leave as 16-byte vector stores; periodic edge points also write their
 //     wrap-around images so the next step streams plain rows.
 // Tap order and arithmetic follow the reference bit for bit (ps_arith.cuh).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -116,6 +117,11 @@ struct StreamParams {
   int32_t rlo, rhi;        // rows this launch updates
   int32_t row_images;      // periodic, single slab: also write wrapped row images
   int32_t nstrips, rc, ntiles;
+  // row slabs with in-kernel halo delivery: the first/last R output rows are also
+  // stored into the neighbours' ghost rows (peer pointers to their u^{k+1} origins)
+  void* halo_up;           // neighbour above: rows [0,R) -> its rows [up_rows, up_rows+R)
+  void* halo_dn;           // neighbour below: rows [rows-R,rows) -> its rows [-R, 0)
+  int32_t up_rows;
   double c[PS_MAX_TAPS];
   float cf[PS_MAX_TAPS];
 };
@@ -299,6 +305,23 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       for (int v = 0; v < V; ++v)
         if (jv + v < p.cols) dst[v] = out[v];
     }
+    if constexpr (!PER) {
+      // in-kernel halo delivery over NVLink (peer-mapped pointers; plain stores)
+      T* peer = nullptr;
+      if (i < R && p.halo_up)
+        peer = static_cast<T*>(p.halo_up) + int64_t(p.up_rows + i) * pitch + jv;
+      else if (i >= p.rows - R && p.halo_dn)
+        peer = static_cast<T*>(p.halo_dn) + int64_t(i - p.rows) * pitch + jv;
+      if (peer) {
+        if (jv + V <= p.cols) {
+          *reinterpret_cast<vec_t*>(peer) = Vec<T>::pack(out);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (jv + v < p.cols) peer[v] = out[v];
+        }
+      }
+    }
     if constexpr (PER) {
       const bool erow = p.row_images && ((i < R) || (i >= p.rows - R));
       const bool ecol = (jv < R) || (jv + V > p.cols - R);
@@ -372,6 +395,9 @@ struct GenParams {
   int64_t pitch;
   int32_t rows, cols, ring, radius;
   int32_t row0, grows, rlo, rhi, row_images;
+  void* halo_up;
+  void* halo_dn;
+  int32_t up_rows;
   double tau;
   float tauf;
   GenTable ta, tb;
@@ -409,6 +435,12 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ GenPara
                               (j < p.cols - p.ring));
       if (!in) {
         out[o] = T(0);
+        if constexpr (!PER) {
+          if (i < p.radius && p.halo_up)
+            static_cast<T*>(p.halo_up)[int64_t(p.up_rows + i) * pitch + j] = T(0);
+          else if (i >= p.rows - p.radius && p.halo_dn)
+            static_cast<T*>(p.halo_dn)[int64_t(i - p.rows) * pitch + j] = T(0);
+        }
         continue;
       }
       const auto acc = gen_acc<T, A>(p.ta, ua, pitch, i, j);
@@ -424,6 +456,12 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ GenPara
         val = Ar::two(acc, ub[o]);
       }
       out[o] = val;
+      if constexpr (!PER) {
+        if (i < p.radius && p.halo_up)
+          static_cast<T*>(p.halo_up)[int64_t(p.up_rows + i) * pitch + j] = val;
+        else if (i >= p.rows - p.radius && p.halo_dn)
+          static_cast<T*>(p.halo_dn)[int64_t(i - p.rows) * pitch + j] = val;
+      }
       if constexpr (PER) {
         const int R = p.radius;
         if ((p.row_images && (i < R || i >= p.rows - R)) || j < R || j >= p.cols - R) {
@@ -585,10 +623,19 @@ static dim3 gen_grid(int64_t rows, int64_t cols) {
 
 static bool single_slab(const ps_grid* g) { return g->row0 == 0 && g->grows == g->rows; }
 
+// Peer halo targets of a row-slab update (logical-origin pointers of the neighbours'
+// u^{k+1} levels; null = no neighbour / exchange done elsewhere).
+struct Halo {
+  void* up = nullptr;
+  void* dn = nullptr;
+  int32_t up_rows = 0;
+};
+
 template <typename T, int A, bool PER, bool FIRST>
 static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, void* out,
                                 const ps_table* ta, const ps_table* tb, double tau,
-                                int64_t rlo, int64_t rhi, cudaStream_t st) {
+                                int64_t rlo, int64_t rhi, cudaStream_t st,
+                                const Halo& h = Halo{}) {
   GenParams p;
   std::memset(&p, 0, sizeof(p));
   p.a = at_origin<T>(g, a);
@@ -604,6 +651,9 @@ static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, 
   p.rlo = int32_t(rlo);
   p.rhi = int32_t(rhi);
   p.row_images = (PER && single_slab(g)) ? 1 : 0;
+  p.halo_up = h.up;
+  p.halo_dn = h.dn;
+  p.up_rows = h.up_rows;
   p.tau = tau;
   p.tauf = static_cast<float>(tau);
   fill_gen_table(p.ta, ta);
@@ -616,7 +666,8 @@ static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, 
 
 template <typename T, int A, class S, bool PER>
 static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
-                               const ps_table* t, int64_t rlo, int64_t rhi, cudaStream_t st) {
+                               const ps_table* t, int64_t rlo, int64_t rhi, cudaStream_t st,
+                               const Halo& h) {
   constexpr int NW = PS_NW;
   constexpr int RB = (S::R == 1) ? PS_RB1 : PS_RB2;
   constexpr int NS = PS_NS;
@@ -644,6 +695,9 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.rlo = int32_t(rlo);
   p.rhi = int32_t(rhi);
   p.row_images = (PER && single_slab(g)) ? 1 : 0;
+  p.halo_up = h.up;
+  p.halo_dn = h.dn;
+  p.up_rows = h.up_rows;
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -676,38 +730,40 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
 
 template <typename T, int A, bool PER>
 static ps_status dispatch_two_step(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
-                                   const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st) {
+                                   const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,
+                                   const Halo& h) {
   // The streaming kernel wants >= 4 rows/cols and at least one wrap (n >= R) for images.
   const bool small = g->rows < 4 || g->cols < 4;
   if (!small && env_int("PS_FORCE_GENERIC", 0) == 0) {
     if (shape_matches<ShapeP5>(t))
-      return launch_stream<T, A, ShapeP5, PER>(g, uk, ukm1, ukp1, t, lo, hi, st);
+      return launch_stream<T, A, ShapeP5, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
     if (shape_matches<ShapeP9>(t))
-      return launch_stream<T, A, ShapeP9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st);
+      return launch_stream<T, A, ShapeP9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
     if (shape_matches<ShapeC9>(t))
-      return launch_stream<T, A, ShapeC9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st);
+      return launch_stream<T, A, ShapeC9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
     if (shape_matches<ShapeP13>(t))
-      return launch_stream<T, A, ShapeP13, PER>(g, uk, ukm1, ukp1, t, lo, hi, st);
+      return launch_stream<T, A, ShapeP13, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
   }
-  return launch_generic<T, A, PER, false>(g, uk, ukm1, ukp1, t, nullptr, 0.0, lo, hi, st);
+  return launch_generic<T, A, PER, false>(g, uk, ukm1, ukp1, t, nullptr, 0.0, lo, hi, st, h);
 }
 
 template <typename T, int A>
 static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const void* ukm1,
                                       void* ukp1, const ps_table* t, int64_t lo, int64_t hi,
-                                      cudaStream_t st) {
+                                      cudaStream_t st, const Halo& h) {
   if (g->bc == PS_BC_PERIODIC)
-    return dispatch_two_step<T, A, true>(g, uk, ukm1, ukp1, t, lo, hi, st);
-  return dispatch_two_step<T, A, false>(g, uk, ukm1, ukp1, t, lo, hi, st);
+    return dispatch_two_step<T, A, true>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+  return dispatch_two_step<T, A, false>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
 }
 
 static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
-                               const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st) {
+                               const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,
+                               const Halo& h = Halo{}) {
   if (g->dtype == PS_F64)
-    return dispatch_two_step_bc<double, ARITH_REF>(g, uk, ukm1, ukp1, t, lo, hi, st);
+    return dispatch_two_step_bc<double, ARITH_REF>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
   if (g->arith == PS_ARITH_NATIVE)
-    return dispatch_two_step_bc<float, ARITH_NATIVE>(g, uk, ukm1, ukp1, t, lo, hi, st);
-  return dispatch_two_step_bc<float, ARITH_REF>(g, uk, ukm1, ukp1, t, lo, hi, st);
+    return dispatch_two_step_bc<float, ARITH_NATIVE>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+  return dispatch_two_step_bc<float, ARITH_REF>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -1069,6 +1125,69 @@ ps_status ps_two_step_rows(const ps_grid* g, const void* uk, const void* ukm1, v
   if ((s = check_table(g, t)) != PS_OK) return s;
   if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(ukp1)) return PS_ERR_ALIGN;
   return two_step_impl(g, uk, ukm1, ukp1, t, row_lo, row_hi, static_cast<cudaStream_t>(stream));
+}
+
+ps_status ps_two_step_halo(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                           const ps_table* t, int64_t row_lo, int64_t row_hi, void* up_ukp1,
+                           int64_t up_rows, void* dn_ukp1, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!uk || !ukm1 || !ukp1 || ukp1 == uk) return PS_ERR_ARG;
+  if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) return PS_ERR_ARG;
+  if (g->bc != PS_BC_DIRICHLET) return PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  if (up_ukp1 && (up_rows < table_radius(t) || !aligned16(up_ukp1))) return PS_ERR_ARG;
+  if (dn_ukp1 && !aligned16(dn_ukp1)) return PS_ERR_ALIGN;
+  if (table_radius(t) > g->rows) return PS_ERR_SHAPE;
+  if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(ukp1)) return PS_ERR_ALIGN;
+  const size_t esz = g->dtype == PS_F64 ? 8 : 4;
+  Halo h;
+  h.up = up_ukp1 ? static_cast<char*>(up_ukp1) + g->origin * esz : nullptr;
+  h.dn = dn_ukp1 ? static_cast<char*>(dn_ukp1) + g->origin * esz : nullptr;
+  h.up_rows = int32_t(up_rows);
+  return two_step_impl(g, uk, ukm1, ukp1, t, row_lo, row_hi, static_cast<cudaStream_t>(stream),
+                       h);
+}
+
+ps_status ps_ipc_get_handle(const void* dev_ptr, void* handle64, int64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return PS_ERR_ARG;
+  // IPC handles name whole allocations; a pointer from a caching allocator may sit
+  // inside a larger block, so report its offset from the allocation base.
+  // (driver entry point fetched at run time: libps.so must load on hosts without a driver)
+  using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static AddrRangeFn addr_range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<AddrRangeFn>(fn);
+  }();
+  if (!addr_range) return PS_ERR_CUDA;
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (addr_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return PS_ERR_CUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return PS_ERR_CUDA;
+  std::memcpy(handle64, &h, sizeof(h));
+  *offset = int64_t(reinterpret_cast<uintptr_t>(dev_ptr) - uintptr_t(base));
+  return PS_OK;
+}
+
+ps_status ps_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return PS_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  if (cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return PS_ERR_CUDA;
+  return PS_OK;
+}
+
+ps_status ps_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return PS_ERR_ARG;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? PS_OK : PS_ERR_CUDA;
 }
 
 ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,

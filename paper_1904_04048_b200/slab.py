@@ -86,10 +86,19 @@ def rows_view(level: nat.Level, first: int, count: int):
 
 
 class VirtualSlabs:
-    """P Dirichlet row slabs of one (n+1)^2 grid on one device (test vehicle)."""
+    """P Dirichlet row slabs of one (n+1)^2 grid on one device (test vehicle).
+
+    ``transport="copy"`` moves halo rows with device copies after each step;
+    ``transport="kernel"`` has each slab's update kernel store its boundary rows straight
+    into the neighbours' ghost rows (``ps_two_step_halo``) — the same code path the
+    multi-GPU p2p transport drives with peer-mapped pointers."""
 
     def __init__(self, scheme, n: int, lam: float, P: int, ring: int | None = None,
-                 dtype: str = "f64", arith: str = "ref", c: float = 1.0):
+                 dtype: str = "f64", arith: str = "ref", c: float = 1.0,
+                 transport: str = "copy"):
+        if transport not in ("copy", "kernel"):
+            raise ValueError(f"transport must be 'copy' or 'kernel', got {transport!r}")
+        self.transport = transport
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         self.n, self.lam, self.P = int(n), float(lam), int(P)
         self.tau = self.lam / self.n / c
@@ -129,9 +138,17 @@ class VirtualSlabs:
         for _ in range(nsteps):
             cur = self.newest
             nxt, prev = (cur + 1) % 3, (cur + 2) % 3
-            for g, lv in zip(self.grids, self.levels):
-                nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
-            self._exchange(nxt)
+            for p, (g, lv) in enumerate(zip(self.grids, self.levels)):
+                if self.transport == "copy":
+                    nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
+                    continue
+                up = self.levels[p - 1][nxt].ptr.value if p > 0 else None
+                dn = self.levels[p + 1][nxt].ptr.value if p + 1 < self.P else None
+                up_rows = self.plans[p - 1].rows if p > 0 else 0
+                nat.two_step_halo(g, lv[cur], lv[prev], lv[nxt], self.t_two, 0, g.rows, up,
+                                  up_rows, dn)
+            if self.transport == "copy":
+                self._exchange(nxt)
             self.newest = nxt
 
     def field(self) -> np.ndarray:
@@ -149,9 +166,12 @@ class DistributedSlabs:
 
     def __init__(self, scheme, n: int, lam: float, ring: int | None = None, dtype: str = "f64",
                  arith: str = "ref", c: float = 1.0, group=None, device=None, compute=None,
-                 level_factory=None):
+                 level_factory=None, transport: str = "nccl"):
         import torch.distributed as dist
 
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        self.transport = transport
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
@@ -172,6 +192,55 @@ class DistributedSlabs:
         self.compute = compute or _KernelCompute(self.spec, self.lam, self.tau)
         self.newest = None
         self._streams = None
+        self._peer = None
+        if transport == "p2p":
+            self._open_peers()
+
+    # -- p2p transport: neighbours' levels mapped through CUDA IPC ------------------------
+    def _open_peers(self):
+        """Exchange IPC handles of the three levels; map the up/down neighbours' levels."""
+        mine = [nat.ipc_handle(lv.ptr.value) for lv in self.levels]
+        allh = [None] * self.P
+        self.dist.all_gather_object(allh, (self.plan.rows, mine), group=self.group)
+        peer = {"up": None, "dn": None, "up_rows": 0, "opened": []}
+        for side, r in (("up", self.plan.up), ("dn", self.plan.down)):
+            if r is None:
+                continue
+            rows, handles = allh[r]
+            ptrs = []
+            for h, off in handles:
+                base = nat.ipc_open(h)
+                peer["opened"].append(base)
+                ptrs.append(base + off)
+            peer[side] = ptrs
+            if side == "up":
+                peer["up_rows"] = rows
+        self._peer = peer
+        import torch
+
+        self._tok = torch.zeros(4, dtype=torch.int32, device=self.levels[0].buf.device)
+
+    def _token_exchange(self):
+        """Tiny send/recv with each neighbour: orders my next step after their boundary
+        kernels (whose stores into my ghost rows then have landed)."""
+        ops = []
+        t = self._tok
+        for i, (peer, _, _) in enumerate(self.plan.recvs):
+            ops.append(self.dist.P2POp(self.dist.irecv, t[i:i + 1], peer, self.group))
+        for i, (peer, _, _) in enumerate(self.plan.sends):
+            ops.append(self.dist.P2POp(self.dist.isend, t[2 + i:3 + i], peer, self.group))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def close(self):
+        if self._peer:
+            for base in self._peer["opened"]:
+                try:
+                    nat.ipc_close(base)
+                except Exception:
+                    pass
+            self._peer = None
 
     # -- transport ---------------------------------------------------------------------
     def _p2p_ops(self, idx: int):
@@ -223,12 +292,25 @@ class DistributedSlabs:
                 self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
             comm, ev_edge, ev_comm = self._streams
             main = torch.cuda.current_stream()
-            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, R)
-            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows)
+            if self.transport == "p2p":
+                # boundary rows land in the neighbours' ghost rows from inside the kernel
+                pr = self._peer
+                up = pr["up"][nxt] if pr["up"] else None
+                dn = pr["dn"][nxt] if pr["dn"] else None
+                c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], 0, R, up, pr["up_rows"],
+                                dn)
+                c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows, up,
+                                pr["up_rows"], dn)
+            else:
+                c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, R)
+                c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows)
             ev_edge.record(main)
             with torch.cuda.stream(comm):
                 comm.wait_event(ev_edge)
-                self.exchange(nxt)
+                if self.transport == "p2p":
+                    self._token_exchange()
+                else:
+                    self.exchange(nxt)
                 ev_comm.record(comm)
             c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], R, rows - R)
             main.wait_event(ev_comm)
@@ -260,3 +342,7 @@ class _KernelCompute:
     def two_step_rows(self, grid, uk, ukm1, out, lo, hi):
         if hi > lo:
             nat.two_step_rows(grid, uk, ukm1, out, self.t_two, lo, hi)
+
+    def two_step_halo(self, grid, uk, ukm1, out, lo, hi, up_ptr, up_rows, dn_ptr):
+        if hi > lo:
+            nat.two_step_halo(grid, uk, ukm1, out, self.t_two, lo, hi, up_ptr, up_rows, dn_ptr)

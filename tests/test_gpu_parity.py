@@ -213,11 +213,12 @@ def test_row_range_and_virtual_slabs_bitwise(nat, oracle, ps):
                            0.4 / n, "dirichlet", 2)
     want, _ = oracle.march(o1, u0, pairs(spec, "two_step", 0.4), steps, "dirichlet", 2)
     for P in (1, 2, 3, 4, 8):
-        vs = VirtualSlabs(spec, n, 0.4, P, ring=2)
-        vs.load_initial(u0, v0)
-        vs.first_step()
-        vs.march(steps)
-        assert same_bits(vs.field(), want), P
+        for transport in ("copy", "kernel"):
+            vs = VirtualSlabs(spec, n, 0.4, P, ring=2, transport=transport)
+            vs.load_initial(u0, v0)
+            vs.first_step()
+            vs.march(steps)
+            assert same_bits(vs.field(), want), (P, transport)
 
 
 def test_gaussian_initial_data_matches_numpy(oracle):
