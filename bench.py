@@ -393,7 +393,7 @@ def gpu_arm_dist(args, cfg, cfg_name):
     if cfg["bc"] != "dirichlet" or not isinstance(cfg["ic"], tuple):
         raise SystemExit("multi-GPU bench supports the Dirichlet Gaussian configs (C3-C5)")
     slab = DistributedSlabs(cfg["scheme"], cfg["n"], cfg["lam"], ring=cfg["ring"],
-                            dtype=cfg["dtype"], arith=cfg["arith"])
+                            dtype=cfg["dtype"], arith=cfg["arith"], transport=args.transport)
     K0, wmin, wmax, vzero = cfg["ic"]
     rng = np.random.default_rng(0)
     pu = gaussian_params(rng, K0, wmin, wmax)
@@ -405,6 +405,10 @@ def gpu_arm_dist(args, cfg, cfg_name):
         nat.gaussian_sum(slab.grid, slab.levels[0], pv[0], pv[1], pv[2], cfg["n"])
     slab.exchange(1)
     slab.exchange(0)
+    ics = None
+    if not args.no_e2e:  # keep this rank's rows of u0 / v0 for the end-to-end leg
+        ics = (torch.from_numpy(slab.levels[1].download()).pin_memory(),
+               None if vzero else torch.from_numpy(slab.levels[0].download()).pin_memory())
     slab.first_step()
     for _ in range(args.warmup):
         slab.step()
@@ -426,6 +430,7 @@ def gpu_arm_dist(args, cfg, cfg_name):
     ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
+    e2e = None if args.no_e2e else e2e_dist(args, cfg, slab, dist, ics)
     inner = cfg["n"] + 1 - 2 * cfg["ring"]
     lup_step = inner * inner
     value = lup_step * K / (total_ms * 1e-3) / 1e9
@@ -440,18 +445,56 @@ def gpu_arm_dist(args, cfg, cfg_name):
             "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
             "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
                        "lambda": cfg["lam"], "arith": cfg["arith"],
-                       "parallelism": f"row slabs x{world}, {slab.R}-row halo over NCCL send/recv "
-                                      "overlapped with the interior update",
+                       "parallelism": f"row slabs x{world}, {slab.R}-row halo "
+                                      + ("over NCCL send/recv" if args.transport == "nccl" else
+                                         "stored into peer ghost rows by the kernel (CUDA IPC)")
+                                      + ", overlapped with the interior update",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(cfg_name),
                          "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)"},
             "clocks": clk.summary(),
             "gpu_launches": launches,
-            "e2e": None,
+            "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def e2e_dist(args, cfg, slab, dist, ics):
+    """Per rank: own rows of u0 (and v0) from pinned host -> device, halo exchange, first
+    step, K-1 steps, own rows of u^K -> pinned host; time = max over ranks."""
+    import torch
+
+    u_host, v_host = ics
+    out = torch.empty_like(u_host).pin_memory()
+    K = args.steps
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    slab.levels[1].view().copy_(u_host, non_blocking=True)
+    if v_host is None:
+        slab.levels[0].buf.zero_()
+    else:
+        slab.levels[0].view().copy_(v_host, non_blocking=True)
+    slab.exchange(1)
+    slab.exchange(0)
+    slab.first_step()
+    for _ in range(K - 1):
+        slab.step()
+    out.copy_(slab.levels[slab.newest].view(), non_blocking=True)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    inner = cfg["n"] + 1 - 2 * cfg["ring"]
+    h2d = u_host.numel() * u_host.element_size() * (1 if v_host is None else 2)
+    return {"value": inner * inner * K / (float(ms.item()) * 1e-3) / 1e9, "unit": "GLUP/s",
+            "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": out.numel() * out.element_size() / K,
+            "what": "per rank: own rows of u0[,v0] pinned host->device, halo exchange, first "
+                    "step, K-1 steps, own rows of u^K -> pinned host; max over ranks "
+                    "(bytes per rank)"}
 
 
 def main():
@@ -464,6 +507,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
+                    help="multi-GPU halo transport")
     ap.add_argument("--tsteps", type=int, default=1, choices=(1, 2, 4),
                     help="temporal blocking depth (Dirichlet configs)")
     args = ap.parse_args()
