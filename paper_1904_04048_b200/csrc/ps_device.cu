@@ -122,6 +122,10 @@ struct StreamParams {
   void* halo_up;           // neighbour above: rows [0,R) -> its rows [up_rows, up_rows+R)
   void* halo_dn;           // neighbour below: rows [rows-R,rows) -> its rows [-R, 0)
   int32_t up_rows;
+  // periodic images: 1 = read u^{k-1} at each image position (the drop-in's possibly
+  // inconsistent alias, simulator.py:184); 0 = images of u^{k-1} are copies of its core
+  // (every level the march produces), so the image value equals the core value
+  int32_t img_exact;
   double c[PS_MAX_TAPS];
   float cf[PS_MAX_TAPS];
 };
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
               const int jj = j + b * p.cols;
               if (ii < -R || ii >= p.rows + R || jj < -R || jj >= p.cols + R) continue;
               const int64_t o = int64_t(ii) * pitch + jj;
-              ukp1[o] = Ar::two(acc[v], ukm1[o]);
+              ukp1[o] = p.img_exact ? Ar::two(acc[v], ukm1[o]) : out[v];
             }
         }
       }
@@ -629,6 +633,7 @@ struct Halo {
   void* up = nullptr;
   void* dn = nullptr;
   int32_t up_rows = 0;
+  bool img_consistent = false;  // periodic input images are copies of the core (march)
 };
 
 template <typename T, int A, bool PER, bool FIRST>
@@ -698,6 +703,7 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.halo_up = h.up;
   p.halo_dn = h.dn;
   p.up_rows = h.up_rows;
+  p.img_exact = h.img_consistent ? 0 : 1;
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -716,6 +722,8 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
     rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
     rc = std::max(rc, std::max(16, 8 * S::R));
     rc = std::min(rc, 128);
+    // small grids (L2-resident, latency-bound): more, shorter tiles beat fewer halo rows
+    if (p.nstrips * ((nrows + rc - 1) / rc) < resident) rc = std::max(4, 2 * S::R);
   }
   rc = int(std::min<int64_t>(rc, nrows));
   p.rc = rc;
@@ -768,24 +776,42 @@ static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Inside a march every periodic level was produced by this library (images = core copies).
+static Halo march_opts() {
+  Halo h;
+  h.img_consistent = true;
+  return h;
+}
+
 // ---------------------------------------------------------------------------
 // Temporal blocking (ps_tblock.cuh)
 // ---------------------------------------------------------------------------
+// Geometry (measured on B200, profiles/ and DESIGN.md): 4 consumer warps x 3 stages,
+// except f32 at depth 4, whose ~224-register windows allow one block per SM — there 8
+// warps x 2 stages keep more warps resident.  Tuning builds override with -D.
 #ifndef PS_TB_NW
-#define PS_TB_NW 4
+#define PS_TB_NW 0
 #endif
 #ifndef PS_TB_RB
 #define PS_TB_RB 0  // 0: 2R+1 rows per stage, so a stage is one full window rotation
 #endif
 #ifndef PS_TB_NS
-#define PS_TB_NS 4
+#define PS_TB_NS 0
 #endif
+template <typename T, int TS>
+constexpr int tb_nw() {
+  return PS_TB_NW > 0 ? PS_TB_NW : ((TS == 4 && sizeof(T) == 4) ? 8 : 4);
+}
+template <typename T, int TS>
+constexpr int tb_ns() {
+  return PS_TB_NS > 0 ? PS_TB_NS : ((TS == 4 && sizeof(T) == 4) ? 2 : 3);
+}
 
 template <typename T, int A, class S, int TS>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st) {
-  constexpr int NW = PS_TB_NW, NS = PS_TB_NS;
+  constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
   auto kern = k_two_step_tb<T, A, S, TS, NW, RB, NS>;
@@ -931,7 +957,8 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
   int c = cur;
   ps_status st = PS_OK;
   for (int k = 0; k < 3 && st == PS_OK; ++k) {
-    st = two_step_impl(g, lvl[c], lvl[(c + 2) % 3], lvl[(c + 1) % 3], t, 0, g->rows, cs);
+    st = two_step_impl(g, lvl[c], lvl[(c + 2) % 3], lvl[(c + 1) % 3], t, 0, g->rows, cs,
+                       march_opts());
     c = (c + 1) % 3;
   }
   cudaGraph_t graph = nullptr;
@@ -1214,7 +1241,8 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
   for (; k < nsteps; ++k) {
     const int prev = (cur + 2) % 3;
     const int next = (cur + 1) % 3;
-    if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st)) != PS_OK)
+    if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st, march_opts()))
+        != PS_OK)
       return s;
     cur = next;
   }
