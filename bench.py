@@ -37,16 +37,16 @@ CONFIGS = {
                steps=1000, ic="standing",
                desc="C2: P9 9-point, 4096^2 f64 periodic, lambda=0.6, standing wave m=4 n=6, 1000 steps"),
     "C3": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f64", arith="ref", lam=0.4,
-               steps=500, ic=(32, 0.01, 0.05, False),
+               steps=500, ic=(32, 0.01, 0.05, False), tb=2,
                desc="C3: P13 13-point, 16384^2 f64, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C3f32": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f32", arith="native",
-                  lam=0.4, steps=500, ic=(32, 0.01, 0.05, False),
+                  lam=0.4, steps=500, ic=(32, 0.01, 0.05, False), tb=2,
                   desc="C3: P13 13-point, 16384^2 f32, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C4": dict(scheme="P9", n=32767, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.6,
-               steps=200, ic=(64, 0.01, 0.05, True),
+               steps=200, ic=(64, 0.01, 0.05, True), tb=4,
                desc="C4: P9 9-point, 32768^2 f64, Dirichlet ring 1, lambda=0.6, 200 steps"),
     "C5": dict(scheme="P13", n=65535, bc="dirichlet", ring=2, dtype="f32", arith="native",
-               lam=0.4, steps=100, ic=(128, 0.002, 0.01, False),
+               lam=0.4, steps=100, ic=(128, 0.002, 0.01, False), tb=2,
                desc="C5: P13 13-point, 65536^2 f32, Dirichlet ring 2, lambda=0.4, 100 steps"),
 }
 
@@ -62,8 +62,8 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(cfg_name):
-    path = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}.json")
+def load_traffic(cfg_name, T=1):
+    path = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}" + (f"_T{T}" if T > 1 else "") + ".json")
     try:
         with open(path) as f:
             return json.load(f).get("dram_bytes_per_launch")
@@ -251,67 +251,93 @@ def make_sim(cfg, tsteps=1):
     return sim
 
 
-def gpu_arm_single(args, cfg, cfg_name):
-    import numpy as np
+def measure_march(args, cfg, T):
+    """Build the config's grid, first step, warm up, then time K march steps at temporal
+    blocking depth T with CUDA events on the launching stream."""
     import torch
 
     from paper_1904_04048_b200 import _native as nat
 
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
-    T = args.tsteps
     sim = make_sim(cfg, T)
     sim.first_step()
     stream = torch.cuda.current_stream()
     # warm-up also instantiates ps_march's CUDA graph (captured for runs of >= 6 steps)
-    args.warmup = max(args.warmup, 6)
-    sim.march(args.warmup)
+    warm = max(args.warmup, 6)
+    sim.march(warm)
     torch.cuda.synchronize()
-
-    lup_step = sim.updated_nodes
-    # algorithmic HBM words per update: 3 (read u^k, u^{k-1}; write u^{k+1}); with
-    # temporal blocking depth T one launch reads 2 levels and writes 2 for T updates
-    words_per_lup = 3.0 if T == 1 else 4.0 / T
-    bytes_launch = words_per_lup * T * sim.itemsize * lup_step
     K = args.steps
     t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = nat.launch_count()
     with ClockSampler(gpu_id(0)) as clk:
         torch.cuda.synchronize()
         t_begin.record(stream)
-        sim.march(K)          # K back-to-back two-step launches (graph replay), one stream
+        sim.march(K)          # K updates: back-to-back hot-kernel launches on one stream
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = nat.launch_count() - launches0
     total_ms = t_begin.elapsed_time(t_end)
-    # the timed region holds only the hot-kernel launches, back to back (K/T launches of
-    # T fused updates each)
-    avg_launch_ms = total_ms / K * T
-    value = lup_step * K / (total_ms * 1e-3) / 1e9
+    lup_step = sim.updated_nodes
+    # algorithmic HBM words per update: 3 (read u^k, u^{k-1}; write u^{k+1}); at temporal
+    # blocking depth T one launch reads 2 levels and writes 2 for T updates
+    words_per_lup = 3.0 if T == 1 else 4.0 / T
+    bytes_launch = words_per_lup * T * sim.itemsize * lup_step
+    avg_launch_ms = total_ms / K * T      # K/T launches of T fused updates each
     peak, peak_src = load_peak()
     achieved = bytes_launch / (avg_launch_ms * 1e-3) / 1e9
-    traffic = load_traffic(cfg_name)
+    return {"sim": sim, "T": T, "K": K, "warmup": warm, "total_ms": total_ms,
+            "value": lup_step * K / (total_ms * 1e-3) / 1e9, "launches": launches,
+            "clocks": clk.summary(), "lup_step": lup_step, "words_per_lup": words_per_lup,
+            "bytes_launch": bytes_launch, "avg_launch_ms": avg_launch_ms, "peak": peak,
+            "peak_src": peak_src, "achieved": achieved}
 
+
+def gpu_arm_single(args, cfg, cfg_name):
+    import torch
+
+    torch.cuda.set_device(torch.device("cuda", 0))
+    tb_ok = cfg["bc"] == "dirichlet"
+    # auto: the fastest measured depth per config (DESIGN.md §9), 1 where blocking is n/a
+    T = args.tsteps if args.tsteps > 0 else (cfg.get("tb", 1) if tb_ok else 1)
+    companion = None
+    if T > 1 and args.tsteps == 0:
+        # also time the unblocked march (one update per launch) for the roofline story
+        c1 = measure_march(args, cfg, 1)
+        companion = {"temporal_blocking": 1, "value": c1["value"], "unit": "GLUP/s",
+                     "ms_per_step": c1["total_ms"] / c1["K"],
+                     "roofline_frac": c1["achieved"] / c1["peak"],
+                     "achieved_gbs": c1["achieved"], "clocks": c1["clocks"]}
+        del c1
+        torch.cuda.empty_cache()
+    m = measure_march(args, cfg, T)
+    sim = m["sim"]
+    lup_roofline = m["peak"] / (3 * sim.itemsize)   # HBM-roofline LUP/s of one update
     line = {
-        "metric": METRIC, "value": value, "unit": "GLUP/s", "n_gpus": 1, "steps": K,
-        "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True,
+        "metric": METRIC, "value": m["value"], "unit": "GLUP/s", "n_gpus": 1, "steps": m["K"],
+        "warmup": m["warmup"], "ms_per_step": m["total_ms"] / m["K"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
         "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
                    "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
                    "parallelism": "single GPU", "temporal_blocking": T,
                    "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
-                         "3 levels streamed per step" if sim.level_bytes > 126e6 else
+                         "streamed from HBM every launch" if sim.level_bytes > 126e6 else
                          "grid fits in L2 (latency-bound correctness config)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_launch,
-                     "kernel_ms_per_launch": avg_launch_ms,
-                     "lup_per_launch": lup_step * T, "bytes_per_lup": words_per_lup * sim.itemsize},
-        "clocks": clk.summary(),
-        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": m["achieved"], "peak": m["peak"], "unit": "GB/s",
+                     "frac": m["achieved"] / m["peak"], "traffic": load_traffic(cfg_name, T),
+                     "peak_source": m["peak_src"],
+                     "algorithmic_bytes_per_launch": m["bytes_launch"],
+                     "kernel_ms_per_launch": m["avg_launch_ms"],
+                     "lup_per_launch": m["lup_step"] * T,
+                     "bytes_per_lup": m["words_per_lup"] * sim.itemsize},
+        # BASELINE's "fraction of HBM roofline" in update terms: value / (HBM GB/s / 3 words)
+        "lup_roofline": {"glups": lup_roofline, "frac": m["value"] / lup_roofline,
+                         "note": "single-update roofline (3 words/LUP); temporal blocking "
+                                 "moves 4/T words/LUP, so it can exceed 1"},
+        "clocks": m["clocks"],
+        "gpu_launches": m["launches"],
     }
+    if companion:
+        line["unblocked_companion"] = companion
     if not args.no_e2e:
         line["e2e"] = e2e_single(args, cfg, sim)
     if not args.no_cpu:
@@ -509,8 +535,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
-    ap.add_argument("--tsteps", type=int, default=1, choices=(1, 2, 4),
-                    help="temporal blocking depth (Dirichlet configs)")
+    ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
+                    help="temporal blocking depth; 0 = the config's measured best (C4: 4, "
+                         "C3/C5: 2, with an unblocked companion measurement; C1/C2: 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

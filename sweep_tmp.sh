@@ -1,4 +1,11 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu6.log 2>&1; echo "exit=$?" >> gpurun_out/pytest_gpu6.log
-for c in C5 C4 C3 C3f32; do for t in 1 2 4; do timeout 200 python bench.py --config $c --tsteps $t --no-e2e --no-cpu > gpurun_out/r6_${c}_T$t.log 2>&1; done; done
-for c in C1 C2; do timeout 200 python bench.py --config $c --no-e2e --no-cpu > gpurun_out/r6_${c}_T1.log 2>&1; done
+B="python bench.py --steps 8 --warmup 6 --no-e2e --no-cpu --tsteps 4"
+$B > gpurun_out/plain_c4t4.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_t4.csv $B > gpurun_out/ncu_launch_c4t4.log 2>&1
+$B > gpurun_out/plain_c4t4b.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_two_step_tb -s 3 -c 1 -o gpurun_out/prof_c4_t4 $B > gpurun_out/ncu_full_c4t4.log 2>&1
+B5="python bench.py --config C5 --steps 8 --warmup 6 --no-e2e --no-cpu --tsteps 2"
+$B5 > gpurun_out/plain_c5t2.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_two_step_tb -s 3 -c 1 -o gpurun_out/prof_c5_t2 $B5 > gpurun_out/ncu_full_c5t2.log 2>&1
+B1="python bench.py --config C5 --steps 8 --warmup 6 --no-e2e --no-cpu --tsteps 1"
+$B1 > gpurun_out/plain_c5t1.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_two_step_stream -s 8 -c 1 -o gpurun_out/prof_c5_t1 $B1 > gpurun_out/ncu_full_c5t1.log 2>&1
+timeout 400 python bench.py > gpurun_out/bench_default3.log 2>&1
+timeout 400 python bench.py --config C5 > gpurun_out/bench_c5_auto.log 2>&1
+timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref3.log 2>&1
