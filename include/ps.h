@@ -172,6 +172,13 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
 ps_status ps_two_step_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                          void* out_last, const ps_table* t, int32_t tsteps, void* stream);
 
+/* ps_two_step_tb restricted to output rows [row_lo, row_hi) of a row slab (boundary rows
+ * first, halo exchange, interior concurrently).  A slab needs ghost >= R*tsteps rows
+ * holding the neighbours' last R*tsteps rows of u^k and R*(tsteps-1) rows of u^{k-1}. */
+ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1,
+                              void* out_prev, void* out_last, const ps_table* t, int32_t tsteps,
+                              int64_t row_lo, int64_t row_hi, void* stream);
+
 /* nsteps updates over four rotating levels with temporal blocking depth tsteps (1, 2, 4);
  * lvl[*newest] = u^k and lvl[*previous] = u^{k-1} on entry and on return.  nsteps not
  * divisible by tsteps finishes with single steps. */

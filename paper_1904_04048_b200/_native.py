@@ -50,7 +50,8 @@ class PsTable(ctypes.Structure):
 
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
-           "ps_march", "ps_two_step_tb", "ps_march_tb", "ps_two_step_halo", "ps_ipc_get_handle",
+           "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_two_step_halo",
+           "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
            "ps_launch_count", "ps_strerror", "ps_version")
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH):
             "ps_march": (i32, [G, ctypes.POINTER(vp), i64, T, ctypes.POINTER(i32), vp]),
             "ps_two_step_tb": (i32, [G, vp, vp, vp, vp, T, i32, vp]),
             "ps_two_step_halo": (i32, [G, vp, vp, vp, T, i64, i64, vp, i64, vp, vp]),
+            "ps_two_step_tb_rows": (i32, [G, vp, vp, vp, vp, T, i32, i64, i64, vp]),
             "ps_ipc_get_handle": (i32, [vp, vp, ctypes.POINTER(i64)]),
             "ps_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
             "ps_ipc_close": (i32, [vp]),
@@ -270,6 +272,14 @@ def two_step_tb(grid, uk: Level, ukm1: Level, out_prev: Level, out_last: Level, 
     check(load_library().ps_two_step_tb(ctypes.byref(grid), uk.ptr, ukm1.ptr, out_prev.ptr,
                                         out_last.ptr, ctypes.byref(t), int(tsteps),
                                         stream or current_stream()), "ps_two_step_tb")
+
+
+def two_step_tb_rows(grid, uk: Level, ukm1: Level, out_prev: Level, out_last: Level,
+                     t: PsTable, tsteps: int, lo: int, hi: int, stream=None):
+    check(load_library().ps_two_step_tb_rows(ctypes.byref(grid), uk.ptr, ukm1.ptr, out_prev.ptr,
+                                             out_last.ptr, ctypes.byref(t), int(tsteps), int(lo),
+                                             int(hi), stream or current_stream()),
+          "ps_two_step_tb_rows")
 
 
 def march_tb(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, previous: int,

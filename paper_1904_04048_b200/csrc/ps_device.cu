@@ -176,6 +176,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();                 // predecessor's levels complete and visible
+  pdl_launch_dependents();    // successor may start its prologue as our blocks drain
 
   const T* __restrict__ uk = static_cast<const T*>(p.uk);
   const T* __restrict__ ukm1 = static_cast<const T*>(p.ukm1);
@@ -467,7 +469,9 @@ __global__ void __launch_bounds__(256) k_generic(const __grid_constant__ GenPara
           static_cast<T*>(p.halo_dn)[int64_t(i - p.rows) * pitch + j] = val;
       }
       if constexpr (PER) {
-        const int R = p.radius;
+        // images within the stencil radius, and always the first one (the reference's
+        // alias row/col n), even for a radius-0 table
+        const int R = max(p.radius, 1);
         if ((p.row_images && (i < R || i >= p.rows - R)) || j < R || j >= p.cols - R) {
           const int aw = p.row_images ? (R + p.rows - 1) / p.rows : 0;
           const int bw = (R + p.cols - 1) / p.cols;
@@ -571,6 +575,26 @@ static int env_int(const char* name, int dflt) {
 
 static ps_status last_cuda_status() {
   return cudaGetLastError() == cudaSuccess ? PS_OK : PS_ERR_CUDA;
+}
+
+// Launch with programmatic stream serialization (PDL) unless PS_PDL=0: the kernel's
+// blocks may be scheduled while the previous kernel in the stream drains; the kernel
+// itself waits (griddepcontrol.wait) before reading anything the predecessor wrote.
+template <typename Params>
+static cudaError_t launch_pdl(void (*kern)(Params, int), int grid, int block, size_t smem,
+                              cudaStream_t st, const Params& p, int slot) {
+  static const bool pdl = env_int("PS_PDL", 1) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p, slot);
 }
 
 template <typename T>
@@ -731,7 +755,8 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.ntiles = int32_t(nchunks * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
   const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
-  kern<<<grid, (NW + 1) * 32, Gm::smem_bytes, st>>>(p, slot);
+  if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
+    return PS_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return last_cuda_status();
 }
@@ -861,39 +886,44 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
   const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
-  kern<<<grid, (NW + 1) * 32, Gm::smem_bytes, st>>>(p, slot);
+  if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
+    return PS_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return last_cuda_status();
 }
 
 template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
-                             void* ol, const ps_table* t, cudaStream_t st) {
+                             void* ol, const ps_table* t, int64_t lo, int64_t hi,
+                             cudaStream_t st) {
   if (shape_matches<ShapeP5>(t))
-    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
   if (shape_matches<ShapeP9>(t))
-    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
   if (shape_matches<ShapeC9>(t))
-    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
   if (shape_matches<ShapeP13>(t))
-    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, 0, g->rows, st);
+    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
   return PS_ERR_TABLE;
 }
 
 template <int TS>
 static ps_status tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol,
-                         const ps_table* t, cudaStream_t st) {
-  if (g->dtype == PS_F64) return dispatch_tb<double, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, st);
+                         const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st) {
+  if (g->dtype == PS_F64)
+    return dispatch_tb<double, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
   if (g->arith == PS_ARITH_NATIVE)
-    return dispatch_tb<float, ARITH_NATIVE, TS>(g, uk, ukm1, op, ol, t, st);
-  return dispatch_tb<float, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, st);
+    return dispatch_tb<float, ARITH_NATIVE, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+  return dispatch_tb<float, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
 }
 
 static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op,
-                                  void* ol, const ps_table* t, int tsteps, cudaStream_t st) {
+                                  void* ol, const ps_table* t, int tsteps, cudaStream_t st,
+                                  int64_t lo = 0, int64_t hi = -1) {
+  if (hi < 0) hi = g->rows;
   switch (tsteps) {
-    case 2: return tb_impl<2>(g, uk, ukm1, op, ol, t, st);
-    case 4: return tb_impl<4>(g, uk, ukm1, op, ol, t, st);
+    case 2: return tb_impl<2>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    case 4: return tb_impl<4>(g, uk, ukm1, op, ol, t, lo, hi, st);
     default: return PS_ERR_ARG;
   }
 }
@@ -1264,6 +1294,26 @@ ps_status ps_two_step_tb(const ps_grid* g, const void* uk, const void* ukm1, voi
     return PS_ERR_ALIGN;
   return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
                           static_cast<cudaStream_t>(stream));
+}
+
+ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1,
+                              void* out_prev, void* out_last, const ps_table* t, int32_t tsteps,
+                              int64_t row_lo, int64_t row_hi, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!uk || !ukm1 || !out_prev || !out_last) return PS_ERR_ARG;
+  if (out_prev == uk || out_prev == ukm1 || out_last == uk || out_last == ukm1 ||
+      out_prev == out_last)
+    return PS_ERR_ARG;
+  if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) return PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  if (!tb_supported(g, t)) return PS_ERR_ARG;
+  // the fused pass reads R*tsteps halo rows of u^k beyond the launch's row range
+  if (int64_t(table_radius(t)) * tsteps > g->ghost && !single_slab(g)) return PS_ERR_SHAPE;
+  if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(out_prev) || !aligned16(out_last))
+    return PS_ERR_ALIGN;
+  return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
+                          static_cast<cudaStream_t>(stream), row_lo, row_hi);
 }
 
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,

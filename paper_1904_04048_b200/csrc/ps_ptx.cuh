@@ -72,4 +72,12 @@ __device__ __forceinline__ uint64_t l2_policy_evict_normal() {
   return p;
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its prologue
+// while this grid drains (launch_dependents), and make every kernel wait for its
+// predecessor's memory before touching global data (wait).  No-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace ps

@@ -91,6 +91,8 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();
+  pdl_launch_dependents();
 
   const T* __restrict__ uk = static_cast<const T*>(p.uk);
   const T* __restrict__ ukm1 = static_cast<const T*>(p.ukm1);

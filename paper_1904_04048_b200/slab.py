@@ -166,12 +166,19 @@ class DistributedSlabs:
 
     def __init__(self, scheme, n: int, lam: float, ring: int | None = None, dtype: str = "f64",
                  arith: str = "ref", c: float = 1.0, group=None, device=None, compute=None,
-                 level_factory=None, transport: str = "nccl"):
+                 level_factory=None, transport: str = "nccl", tsteps: int = 1):
         import torch.distributed as dist
 
         if transport not in ("nccl", "p2p"):
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
+        if tsteps not in (1, 2, 4):
+            raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
+        if tsteps > 1 and transport != "nccl":
+            raise ValueError("temporal blocking across slabs uses the nccl transport")
         self.transport = transport
+        # Temporal blocking depth T: one pass advances T steps, so the halo is R*T rows of
+        # the newest level and R*(T-1) rows of the one before.
+        self.T = int(tsteps)
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
@@ -184,11 +191,12 @@ class DistributedSlabs:
         self.ring = R if ring is None else int(ring)
         grows = self.n + 1
         self.grows = grows
-        self.plan = SlabPlan.build(grows, self.P, self.rank, R, periodic=False)
-        self.grid = nat.make_slab_grid(grows, grows, self.plan.row0, self.plan.rows, max(2, R),
-                                       self.ring, "dirichlet", dtype, arith)
+        self.plan = SlabPlan.build(grows, self.P, self.rank, R * self.T, periodic=False)
+        self.grid = nat.make_slab_grid(grows, grows, self.plan.row0, self.plan.rows,
+                                       max(2, R * self.T), self.ring, "dirichlet", dtype, arith)
         make = level_factory or (lambda g: nat.Level(g, device=device))
-        self.levels = [make(self.grid) for _ in range(3)]
+        self.levels = [make(self.grid) for _ in range(3 if self.T == 1 else 4)]
+        self.previous = None
         self.compute = compute or _KernelCompute(self.spec, self.lam, self.tau)
         self.newest = None
         self._streams = None
@@ -243,20 +251,29 @@ class DistributedSlabs:
             self._peer = None
 
     # -- transport ---------------------------------------------------------------------
-    def _p2p_ops(self, idx: int):
+    def _p2p_ops(self, idx: int, count: int):
+        """Send my first/last ``count`` rows of level ``idx`` up/down; receive the
+        neighbours' into my ghost rows."""
         ops = []
         lv = self.levels[idx]
-        for peer, first, count in self.plan.recvs:
-            ops.append(self.dist.P2POp(self.dist.irecv, rows_view(lv, first, count), peer,
+        rows = self.plan.rows
+        for peer, first, _ in self.plan.recvs:
+            dst = -count if first < 0 else rows
+            ops.append(self.dist.P2POp(self.dist.irecv, rows_view(lv, dst, count), peer,
                                        self.group))
-        for peer, first, count in self.plan.sends:
-            ops.append(self.dist.P2POp(self.dist.isend, rows_view(lv, first, count), peer,
+        for peer, first, _ in self.plan.sends:
+            src = 0 if first == 0 else rows - count
+            ops.append(self.dist.P2POp(self.dist.isend, rows_view(lv, src, count), peer,
                                        self.group))
         return ops
 
-    def exchange(self, idx: int):
-        """Blocking (w.r.t. the current stream) halo exchange of level ``idx``."""
-        ops = self._p2p_ops(idx)
+    def exchange(self, idx: int, count: int | None = None, idx2: int | None = None,
+                 count2: int = 0):
+        """Blocking (w.r.t. the current stream) halo exchange of level ``idx`` (``count``
+        rows; default the full halo) and optionally ``count2`` rows of level ``idx2``."""
+        ops = self._p2p_ops(idx, self.plan.halo if count is None else count)
+        if idx2 is not None and count2 > 0:
+            ops += self._p2p_ops(idx2, count2)
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
@@ -272,11 +289,13 @@ class DistributedSlabs:
     def first_step(self):
         self.compute.first_step(self.grid, self.levels[1], self.levels[0], self.levels[2])
         self.exchange(2)
-        self.newest = 2
+        self.newest, self.previous = 2, 1
 
     def step(self, overlap: bool = True):
         """One two-step update: boundary rows, then halo exchange on the communication
         stream concurrently with the interior rows."""
+        if self.T > 1:
+            raise RuntimeError("temporally blocked slabs advance with step_block()/march()")
         cur = self.newest
         nxt, prev = (cur + 1) % 3, (cur + 2) % 3
         lv = self.levels
@@ -314,14 +333,50 @@ class DistributedSlabs:
                 ev_comm.record(comm)
             c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], R, rows - R)
             main.wait_event(ev_comm)
-        self.newest = nxt
+        self.newest, self.previous = nxt, cur
+
+    def step_block(self, overlap: bool = True):
+        """One temporally blocked pass: T updates.  Boundary rows (R*T each side) first,
+        then their halo rows of the two newest levels go to the neighbours on the
+        communication stream while the interior rows update."""
+        T, R, rows = self.T, self.R, self.plan.rows
+        cur, prev = self.newest, self.previous
+        f1, f2 = [x for x in range(4) if x not in (cur, prev)]
+        lv, c = self.levels, self.compute
+        H = R * T
+        if self.P == 1 or rows < 3 * H or not overlap or not c.is_cuda:
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, rows)
+            self.exchange(f2, H, f1, R * (T - 1))
+        else:
+            import torch
+
+            if self._streams is None:
+                self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
+            comm, ev_edge, ev_comm = self._streams
+            main = torch.cuda.current_stream()
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H)
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows)
+            ev_edge.record(main)
+            with torch.cuda.stream(comm):
+                comm.wait_event(ev_edge)
+                self.exchange(f2, H, f1, R * (T - 1))
+                ev_comm.record(comm)
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, H, rows - H)
+            main.wait_event(ev_comm)
+        self.newest, self.previous = f2, f1
 
     def march(self, nsteps: int, overlap: bool = True):
-        for _ in range(nsteps):
-            self.step(overlap)
+        if self.T == 1:
+            for _ in range(nsteps):
+                self.step(overlap)
+            return
+        if nsteps % self.T:
+            raise ValueError(f"nsteps={nsteps} must be a multiple of tsteps={self.T}")
+        for _ in range(nsteps // self.T):
+            self.step_block(overlap)
 
     def own_rows(self, which: str = "newest") -> np.ndarray:
-        idx = self.newest if which == "newest" else (self.newest + 2) % 3
+        idx = self.newest if which == "newest" else self.previous
         return self.levels[idx].download()
 
 
@@ -346,3 +401,7 @@ class _KernelCompute:
     def two_step_halo(self, grid, uk, ukm1, out, lo, hi, up_ptr, up_rows, dn_ptr):
         if hi > lo:
             nat.two_step_halo(grid, uk, ukm1, out, self.t_two, lo, hi, up_ptr, up_rows, dn_ptr)
+
+    def tb_rows(self, grid, uk, ukm1, out_prev, out_last, T, lo, hi):
+        if hi > lo:
+            nat.two_step_tb_rows(grid, uk, ukm1, out_prev, out_last, self.t_two, T, lo, hi)

@@ -368,3 +368,51 @@ def test_temporal_blocking_large_grid_matches_single_steps():
     for ts in (2, 4):
         assert same_bits(res[ts][0], res[1][0]), ts
         assert same_bits(res[ts][1], res[1][1]), ts
+
+
+# ------------------------------------------------------------ arbitrary tables / tiny grids
+def _reordered(spec):
+    """Same scheme with its tables in reversed dict order (a tap order no specialised
+    kernel knows): the generic kernel must follow it."""
+    from dataclasses import replace
+
+    rev = lambda t: dict(reversed(list(t.items())))  # noqa: E731
+    return replace(spec, name=spec.name + "-rev", first_u=rev(spec.first_u),
+                   first_v=rev(spec.first_v), two_step=rev(spec.two_step))
+
+
+@pytest.mark.parametrize("which", ["P3", "P11", "P1", "P9rev", "P13rev"])
+@pytest.mark.parametrize("bc", ["dirichlet", "periodic"])
+def test_dropin_arbitrary_tables_bitwise(ps, oracle, which, bc):
+    m = {"P3": 5, "P11": 14, "P1": 1}
+    if which in m:
+        spec = ps.generate_scheme(m[which])
+    else:
+        spec = _reordered(ps.named_scheme(which[:-3]))
+    if bc == "dirichlet" and spec.radius > 1:
+        pytest.skip("reference rejects Dirichlet radius > 1")
+    rng = np.random.default_rng(11)
+    for n in (6, 35, 300):
+        a, b = rng.normal(size=(n + 1, n + 1)), rng.normal(size=(n + 1, n + 1))
+        lam, tau = 0.5, 0.5 / n
+        got = ps.two_step(a, b, spec, lam, bc)
+        want = oracle.two_step(a, b, pairs(spec, "two_step", lam), bc, 1)
+        assert same_bits(got, want), (which, bc, n)
+        got = ps.first_step(a, b, spec, lam, tau, bc)
+        want = oracle.first_step(a, b, pairs(spec, "first_u", lam), pairs(spec, "first_v", lam),
+                                 tau, bc, 1)
+        assert same_bits(got, want), (which, bc, n)
+
+
+@pytest.mark.parametrize("name", ["P5", "P9", "P13"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5])
+def test_dropin_tiny_grids_bitwise(ps, oracle, name, n):
+    spec = ps.named_scheme(name)
+    rng = np.random.default_rng(n)
+    a, b = rng.normal(size=(n + 1, n + 1)), rng.normal(size=(n + 1, n + 1))
+    for bc in ("dirichlet", "periodic"):
+        if bc == "dirichlet" and spec.radius > 1:
+            continue
+        got = ps.two_step(a, b, spec, 0.5, bc)
+        want = oracle.two_step(a, b, pairs(spec, "two_step", 0.5), bc, 1)
+        assert same_bits(got, want), (name, n, bc)

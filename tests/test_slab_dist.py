@@ -91,8 +91,21 @@ class OracleCompute:
                           rows=(grid.row0 + lo, grid.row0 + hi))
         out.view()[lo:hi].copy_(torch.from_numpy(full[grid.row0 + lo:grid.row0 + hi]))
 
+    def tb_rows(self, grid, uk, ukm1, out_prev, out_last, T, lo, hi):
+        """T fused updates of rows [lo, hi): T oracle steps on the embedded slab (its
+        ghost rows hold the neighbours' R*T / R*(T-1) halo rows)."""
+        from oracle import oracle as O
 
-def _worker(rank, world, port, scheme, n, lam, ring, steps, dtype, outdir):
+        if hi <= lo:
+            return
+        last, prev = O.march(self._embed(uk), self._embed(ukm1), self.two, T, "dirichlet",
+                             self.ring)
+        a, b = grid.row0 + lo, grid.row0 + hi
+        out_last.view()[lo:hi].copy_(torch.from_numpy(last[a:b]))
+        out_prev.view()[lo:hi].copy_(torch.from_numpy(prev[a:b]))
+
+
+def _worker(rank, world, port, scheme, n, lam, ring, steps, dtype, outdir, tsteps=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -103,7 +116,7 @@ def _worker(rank, world, port, scheme, n, lam, ring, steps, dtype, outdir):
         tau = lam / n
         slab = DistributedSlabs(spec, n, lam, ring=ring, dtype=dtype,
                                 compute=OracleCompute(spec, lam, tau, ring),
-                                level_factory=HostLevel)
+                                level_factory=HostLevel, tsteps=tsteps)
         rng = np.random.default_rng(42)
         npdt = np.float64 if dtype == "f64" else np.float32
         u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
@@ -113,6 +126,7 @@ def _worker(rank, world, port, scheme, n, lam, ring, steps, dtype, outdir):
         slab.first_step()
         slab.march(steps)
         np.save(os.path.join(outdir, f"rank{rank}.npy"), slab.own_rows())
+        np.save(os.path.join(outdir, f"prev{rank}.npy"), slab.own_rows("previous"))
     finally:
         dist.destroy_process_group()
 
@@ -123,16 +137,20 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,scheme,ring,dtype", [(2, "P13", 2, "f64"), (3, "P9", 1, "f64"),
-                                                     (2, "P5", 1, "f32")])
-def test_distributed_slabs_gloo_bitwise(world, scheme, ring, dtype):
+@pytest.mark.parametrize("world,scheme,ring,dtype,tsteps", [
+    (2, "P13", 2, "f64", 1), (3, "P9", 1, "f64", 1), (2, "P5", 1, "f32", 1),
+    (2, "P13", 2, "f64", 2), (3, "P9", 1, "f64", 4)])
+def test_distributed_slabs_gloo_bitwise(world, scheme, ring, dtype, tsteps):
     from oracle import oracle as O
 
-    n, lam, steps = 40, 0.4 if scheme == "P13" else 0.6, 5
+    n, lam = 40, 0.4 if scheme == "P13" else 0.6
+    steps = 5 if tsteps == 1 else 2 * tsteps
     with tempfile.TemporaryDirectory() as tmp:
-        mp.spawn(_worker, args=(world, _free_port(), scheme, n, lam, ring, steps, dtype, tmp),
-                 nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), scheme, n, lam, ring, steps, dtype, tmp,
+                                tsteps), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(tmp, f"rank{r}.npy")) for r in range(world)])
+        got_prev = np.concatenate([np.load(os.path.join(tmp, f"prev{r}.npy"))
+                                   for r in range(world)])
     spec = named_scheme(scheme)
     rng = np.random.default_rng(42)
     npdt = np.float64 if dtype == "f64" else np.float32
@@ -140,8 +158,9 @@ def test_distributed_slabs_gloo_bitwise(world, scheme, ring, dtype):
     v0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
     u1 = O.first_step(u0, v0, evaluate_table(spec.first_u, lam), evaluate_table(spec.first_v, lam),
                       lam / n, "dirichlet", ring)
-    want, _ = O.march(u1, u0, evaluate_table(spec.two_step, lam), steps, "dirichlet", ring)
+    want, want_prev = O.march(u1, u0, evaluate_table(spec.two_step, lam), steps, "dirichlet", ring)
     assert got.tobytes() == want.tobytes()
+    assert got_prev.tobytes() == want_prev.tobytes()
 
 
 def test_partition_and_plans():
