@@ -122,6 +122,7 @@ struct StreamParams {
   void* halo_up;           // neighbour above: rows [0,R) -> its rows [up_rows, up_rows+R)
   void* halo_dn;           // neighbour below: rows [rows-R,rows) -> its rows [-R, 0)
   int32_t up_rows;
+  int32_t reverse;          // walk tiles bottom-up (alternate launches: L2 reuse)
   // periodic images: 1 = read u^{k-1} at each image position (the drop-in's possibly
   // inconsistent alias, simulator.py:184); 0 = images of u^{k-1} are copies of its core
   // (every level the march produces), so the image value equals the core value
@@ -194,8 +195,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       uint32_t g = 0;
       int tile = blockIdx.x;
       while (tile < p.ntiles) {
-        const int chunk = tile / p.nstrips;
-        const int strip = tile - chunk * p.nstrips;
+        // reversed launches walk the tiles bottom-up, so the rows the previous launch
+        // wrote last (still in L2) are read first
+        const int tid = p.reverse ? p.ntiles - 1 - tile : tile;
+        const int chunk = tid / p.nstrips;
+        const int strip = tid - chunk * p.nstrips;
         const int i0 = p.rlo + chunk * p.rc;
         const int i1 = min(i0 + p.rc, p.rhi);
         const int j0 = strip * W;
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           const uint32_t s = g % NS;
           const uint32_t k = g / NS;
           if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-          s_tile[s] = tile;
+          s_tile[s] = tid;
           s_mlo[s] = mlo;
           const int mhi = min(mlo + RB, ne);
           const int nk = max(0, mhi - max(mlo, 2 * R));
@@ -658,6 +662,7 @@ struct Halo {
   void* dn = nullptr;
   int32_t up_rows = 0;
   bool img_consistent = false;  // periodic input images are copies of the core (march)
+  bool reverse = false;         // walk tiles bottom-up
 };
 
 template <typename T, int A, bool PER, bool FIRST>
@@ -728,6 +733,7 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.halo_dn = h.dn;
   p.up_rows = h.up_rows;
   p.img_exact = h.img_consistent ? 0 : 1;
+  p.reverse = h.reverse ? 1 : 0;
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -801,10 +807,13 @@ static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Inside a march every periodic level was produced by this library (images = core copies).
-static Halo march_opts() {
+// Inside a march every periodic level was produced by this library (images = core copies);
+// odd steps walk their tiles bottom-up so they start on the rows the previous step wrote
+// last, which grids of a few hundred MB still find in the 126 MB L2.
+static Halo march_opts(int64_t k = 0) {
   Halo h;
   h.img_consistent = true;
+  h.reverse = (k & 1) != 0 && env_int("PS_ALTERNATE", 1) != 0;
   return h;
 }
 
@@ -835,7 +844,7 @@ constexpr int tb_ns() {
 template <typename T, int A, class S, int TS>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool reverse) {
   constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
@@ -867,6 +876,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.gmin = -int32_t(g->ghost);
   p.gmax = int32_t(g->rows + g->ghost);
   p.cmax = int32_t(g->pitch - (g->origin - g->ghost * g->pitch));
+  p.reverse = reverse ? 1 : 0;
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -895,35 +905,35 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
 template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool rev) {
   if (shape_matches<ShapeP5>(t))
-    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeP9>(t))
-    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeC9>(t))
-    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeP13>(t))
-    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   return PS_ERR_TABLE;
 }
 
 template <int TS>
 static ps_status tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol,
-                         const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st) {
+                         const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st, bool rev) {
   if (g->dtype == PS_F64)
-    return dispatch_tb<double, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return dispatch_tb<double, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (g->arith == PS_ARITH_NATIVE)
-    return dispatch_tb<float, ARITH_NATIVE, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
-  return dispatch_tb<float, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    return dispatch_tb<float, ARITH_NATIVE, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+  return dispatch_tb<float, ARITH_REF, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
 }
 
 static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                                   void* ol, const ps_table* t, int tsteps, cudaStream_t st,
-                                  int64_t lo = 0, int64_t hi = -1) {
+                                  int64_t lo = 0, int64_t hi = -1, bool rev = false) {
   if (hi < 0) hi = g->rows;
   switch (tsteps) {
-    case 2: return tb_impl<2>(g, uk, ukm1, op, ol, t, lo, hi, st);
-    case 4: return tb_impl<4>(g, uk, ukm1, op, ol, t, lo, hi, st);
+    case 2: return tb_impl<2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    case 4: return tb_impl<4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
     default: return PS_ERR_ARG;
   }
 }
@@ -935,10 +945,12 @@ static bool tb_supported(const ps_grid* g, const ps_table* t) {
 }
 
 // ---------------------------------------------------------------------------
-// CUDA-graph replay of the march: one rotation cycle (3 two-step launches) is
-// captured once per (grid, levels, table, phase) and replayed nsteps/3 times, which
-// removes per-launch CPU cost and launch gaps on latency-bound grids.
+// CUDA-graph replay of the march: six launches (two level-rotation cycles, so the
+// alternating tile direction lines up too) are captured once per (grid, levels, table,
+// phase) and replayed nsteps/6 times, which removes per-launch CPU cost and launch gaps
+// on latency-bound grids.
 // ---------------------------------------------------------------------------
+constexpr int kGraphCycle = 6;
 struct GraphKey {
   ps_grid g;
   void* lvl[3];
@@ -986,9 +998,9 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
   }
   int c = cur;
   ps_status st = PS_OK;
-  for (int k = 0; k < 3 && st == PS_OK; ++k) {
+  for (int k = 0; k < kGraphCycle && st == PS_OK; ++k) {
     st = two_step_impl(g, lvl[c], lvl[(c + 2) % 3], lvl[(c + 1) % 3], t, 0, g->rows, cs,
-                       march_opts());
+                       march_opts(k));
     c = (c + 1) % 3;
   }
   cudaGraph_t graph = nullptr;
@@ -1001,7 +1013,7 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
     return nullptr;
   }
   cudaGraphDestroy(graph);
-  g_launches.fetch_sub(3, std::memory_order_relaxed);  // captured, not executed
+  g_launches.fetch_sub(kGraphCycle, std::memory_order_relaxed);  // captured, not executed
   GraphEntry& slot = g_graphs[g_graph_next];
   if (g_graph_next < g_ngraphs && slot.exec) cudaGraphExecDestroy(slot.exec);
   slot.key = key;
@@ -1259,20 +1271,20 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int cur = *newest;
   int64_t k = 0;
-  if (nsteps >= 6 && env_int("PS_GRAPH", 1) != 0) {
+  if (nsteps >= 2 * kGraphCycle && env_int("PS_GRAPH", 1) != 0) {
     if (cudaGraphExec_t exec = cycle_graph(g, lvl, cur, t)) {
-      for (; k + 3 <= nsteps; k += 3) {
+      for (; k + kGraphCycle <= nsteps; k += kGraphCycle) {
         if (cudaGraphLaunch(exec, st) != cudaSuccess) return PS_ERR_CUDA;
-        g_launches.fetch_add(3, std::memory_order_relaxed);
+        g_launches.fetch_add(kGraphCycle, std::memory_order_relaxed);
       }
-      // a full cycle returns the rotation to the same phase: cur is unchanged
+      // whole rotation cycles return the levels to the same phase: cur is unchanged
     }
   }
   for (; k < nsteps; ++k) {
     const int prev = (cur + 2) % 3;
     const int next = (cur + 1) % 3;
-    if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st, march_opts()))
-        != PS_OK)
+    if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st,
+                           march_opts(k))) != PS_OK)
       return s;
     cur = next;
   }
@@ -1336,10 +1348,12 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
       if (x != a && x != b) (n++ == 0 ? *f1 : *f2) = x;
   };
   if (tsteps > 1) {
-    for (; k + tsteps <= nsteps; k += tsteps) {
+    const bool alternate = env_int("PS_ALTERNATE", 1) != 0;
+    for (int64_t blk = 0; k + tsteps <= nsteps; k += tsteps, ++blk) {
       int f1, f2;
       free_pair(cur, prev, &f1, &f2);
-      if ((s = two_step_tb_impl(g, lvl[cur], lvl[prev], lvl[f1], lvl[f2], t, tsteps, st)) != PS_OK)
+      if ((s = two_step_tb_impl(g, lvl[cur], lvl[prev], lvl[f1], lvl[f2], t, tsteps, st, 0,
+                                g->rows, alternate && (blk & 1))) != PS_OK)
         return s;
       prev = f1;
       cur = f2;

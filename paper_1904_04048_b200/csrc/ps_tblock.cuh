@@ -32,6 +32,7 @@ struct TBParams {
   int32_t gmin, gmax;      // loadable row range [gmin, gmax) (allocation incl. ghosts)
   int32_t cmax;            // loadable columns: element index < cmax (from logical col 0)
   int32_t nstrips, rc, ntiles;
+  int32_t reverse;         // walk tiles bottom-up (alternate launches: L2 reuse)
   double c[PS_MAX_TAPS];
   float cf[PS_MAX_TAPS];
 };
@@ -108,8 +109,11 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       uint32_t g = 0;
       int tile = blockIdx.x;
       while (tile < p.ntiles) {
-        const int chunk = tile / p.nstrips;
-        const int strip = tile - chunk * p.nstrips;
+        // reversed launches walk the tiles bottom-up, so the rows the previous launch
+        // wrote last (still in L2) are read first
+        const int tid = p.reverse ? p.ntiles - 1 - tile : tile;
+        const int chunk = tid / p.nstrips;
+        const int strip = tid - chunk * p.nstrips;
         const int i0 = p.rlo + chunk * p.rc;
         const int i1 = min(i0 + p.rc, p.rhi);
         const int j0 = strip * W;
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           const uint32_t s = g % NS;
           const uint32_t k = g / NS;
           if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-          s_tile[s] = tile;
+          s_tile[s] = tid;
           s_mlo[s] = mlo;
           const int mhi = min(mlo + RB, ne);
           uint32_t bytes = 0;
