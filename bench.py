@@ -261,8 +261,8 @@ def measure_march(args, cfg, T):
     sim = make_sim(cfg, T)
     sim.first_step()
     stream = torch.cuda.current_stream()
-    # warm-up also instantiates ps_march's CUDA graph (captured for runs of >= 6 steps)
-    warm = max(args.warmup, 6)
+    # warm-up also instantiates ps_march's CUDA graph (captured for runs of >= 12 steps)
+    warm = max(args.warmup, 12)
     sim.march(warm)
     torch.cuda.synchronize()
     K = args.steps

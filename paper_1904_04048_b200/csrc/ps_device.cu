@@ -810,10 +810,18 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // Inside a march every periodic level was produced by this library (images = core copies);
 // odd steps walk their tiles bottom-up so they start on the rows the previous step wrote
 // last, which grids of a few hundred MB still find in the 126 MB L2.
-static Halo march_opts(int64_t k = 0) {
+static bool alternate_walk(const ps_grid* g) {
+  // only grids whose level is within ~2x the L2 keep useful rows between launches
+  // (measured: +4 % on C2's 134 MB levels; on 17 GB levels the reversed walk cost 6 %)
+  static const int mode = env_int("PS_ALTERNATE", -1);
+  if (mode >= 0) return mode != 0;
+  return ps_level_bytes(g) <= (size_t(256) << 20);
+}
+
+static Halo march_opts(const ps_grid* g, int64_t k) {
   Halo h;
   h.img_consistent = true;
-  h.reverse = (k & 1) != 0 && env_int("PS_ALTERNATE", 1) != 0;
+  h.reverse = (k & 1) != 0 && alternate_walk(g);
   return h;
 }
 
@@ -841,14 +849,14 @@ constexpr int tb_ns() {
   return PS_TB_NS > 0 ? PS_TB_NS : ((TS == 4 && sizeof(T) == 4) ? 2 : 3);
 }
 
-template <typename T, int A, class S, int TS>
+template <typename T, int A, class S, int TS, bool PER>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse) {
   constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
-  auto kern = k_two_step_tb<T, A, S, TS, NW, RB, NS>;
+  auto kern = k_two_step_tb<T, A, S, TS, PER, NW, RB, NS>;
   static std::once_flag once;
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {
@@ -868,7 +876,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.pitch = g->pitch;
   p.rows = int32_t(g->rows);
   p.cols = int32_t(g->cols);
-  p.ring = g->ring;
+  p.ring = PER ? 0 : g->ring;
   p.row0 = int32_t(g->row0);
   p.grows = int32_t(g->grows);
   p.rlo = int32_t(rlo);
@@ -907,13 +915,13 @@ static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
                              cudaStream_t st, bool rev) {
   if (shape_matches<ShapeP5>(t))
-    return launch_tb<T, A, ShapeP5, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeP9>(t))
-    return launch_tb<T, A, ShapeP9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeC9>(t))
-    return launch_tb<T, A, ShapeC9, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   if (shape_matches<ShapeP13>(t))
-    return launch_tb<T, A, ShapeP13, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
   return PS_ERR_TABLE;
 }
 
@@ -938,10 +946,15 @@ static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* 
   }
 }
 
-static bool tb_supported(const ps_grid* g, const ps_table* t) {
-  return g->bc == PS_BC_DIRICHLET && g->rows >= 4 && g->cols >= 4 &&
-         (shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) || shape_matches<ShapeC9>(t) ||
-          shape_matches<ShapeP13>(t));
+static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
+  const bool shape = shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) ||
+                     shape_matches<ShapeC9>(t) || shape_matches<ShapeP13>(t);
+  if (!shape || g->rows < 4 || g->cols < 4) return false;
+  if (g->bc == PS_BC_DIRICHLET) return true;
+  // periodic: single slab, images to depth R*tsteps must fit the ghost band, and one
+  // wrap must cover them
+  const int64_t D = int64_t(table_radius(t)) * tsteps;
+  return single_slab(g) && D <= g->ghost && D <= g->rows && D <= g->cols;
 }
 
 // ---------------------------------------------------------------------------
@@ -1000,7 +1013,7 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
   ps_status st = PS_OK;
   for (int k = 0; k < kGraphCycle && st == PS_OK; ++k) {
     st = two_step_impl(g, lvl[c], lvl[(c + 2) % 3], lvl[(c + 1) % 3], t, 0, g->rows, cs,
-                       march_opts(k));
+                       march_opts(g, k));
     c = (c + 1) % 3;
   }
   cudaGraph_t graph = nullptr;
@@ -1284,7 +1297,7 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
     const int prev = (cur + 2) % 3;
     const int next = (cur + 1) % 3;
     if ((s = two_step_impl(g, lvl[cur], lvl[prev], lvl[next], t, 0, g->rows, st,
-                           march_opts(k))) != PS_OK)
+                           march_opts(g, k))) != PS_OK)
       return s;
     cur = next;
   }
@@ -1301,7 +1314,7 @@ ps_status ps_two_step_tb(const ps_grid* g, const void* uk, const void* ukm1, voi
       out_prev == out_last)
     return PS_ERR_ARG;
   if ((s = check_table(g, t)) != PS_OK) return s;
-  if (!tb_supported(g, t)) return PS_ERR_ARG;
+  if (!tb_supported(g, t, tsteps)) return PS_ERR_ARG;
   if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(out_prev) || !aligned16(out_last))
     return PS_ERR_ALIGN;
   return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
@@ -1319,7 +1332,7 @@ ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1
     return PS_ERR_ARG;
   if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) return PS_ERR_ARG;
   if ((s = check_table(g, t)) != PS_OK) return s;
-  if (!tb_supported(g, t)) return PS_ERR_ARG;
+  if (!tb_supported(g, t, tsteps)) return PS_ERR_ARG;
   // the fused pass reads R*tsteps halo rows of u^k beyond the launch's row range
   if (int64_t(table_radius(t)) * tsteps > g->ghost && !single_slab(g)) return PS_ERR_SHAPE;
   if (!aligned16(uk) || !aligned16(ukm1) || !aligned16(out_prev) || !aligned16(out_last))
@@ -1339,16 +1352,22 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
     if (!lvl[x] || !aligned16(lvl[x])) return lvl[x] ? PS_ERR_ALIGN : PS_ERR_ARG;
   if ((s = check_table(g, t)) != PS_OK) return s;
   if (tsteps != 1 && tsteps != 2 && tsteps != 4) return PS_ERR_ARG;
-  if (tsteps > 1 && !tb_supported(g, t)) return PS_ERR_ARG;
+  if (tsteps > 1 && !tb_supported(g, t, tsteps)) return PS_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t k = 0;
+  if (tsteps > 1 && g->bc == PS_BC_PERIODIC && nsteps >= tsteps) {
+    // blocked passes read wrap-around images to depth R*tsteps; levels written by a
+    // single step (first step, earlier remainders) carry them only to depth R
+    if ((s = ps_fill_ghosts(g, lvl[cur], 0, stream)) != PS_OK) return s;
+    if ((s = ps_fill_ghosts(g, lvl[prev], 0, stream)) != PS_OK) return s;
+  }
   auto free_pair = [&](int a, int b, int* f1, int* f2) {
     int n = 0;
     for (int x = 0; x < 4; ++x)
       if (x != a && x != b) (n++ == 0 ? *f1 : *f2) = x;
   };
   if (tsteps > 1) {
-    const bool alternate = env_int("PS_ALTERNATE", 1) != 0;
+    const bool alternate = alternate_walk(g);
     for (int64_t blk = 0; k + tsteps <= nsteps; k += tsteps, ++blk) {
       int f1, f2;
       free_pair(cur, prev, &f1, &f2);

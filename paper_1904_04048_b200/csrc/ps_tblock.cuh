@@ -17,7 +17,8 @@
 //   * every stage re-pins the Dirichlet ring (and zeroes rows/cols outside the grid),
 //     so each intermediate level is exactly what TS separate launches would produce —
 //     results are bitwise equal to the unblocked march.
-// Dirichlet grids only (periodic images would need per-level wrap handling).
+// Periodic grids: the ghost rows/cols of both inputs must hold wrap-around images to
+// depth R*TS (ps_fill_ghosts, or a previous blocked pass, which refreshes them).
 #pragma once
 // (included inside namespace ps, after the streaming kernel's helpers)
 
@@ -61,7 +62,7 @@ __device__ __forceinline__ T shfl_down1(T x) {
   return __shfl_down_sync(0xffffffffu, x, 1);
 }
 
-template <typename T, int A, class S, int TS, int NW, int RB, int NS>
+template <typename T, int A, class S, int TS, bool PER, int NW, int RB, int NS>
 __global__ void __launch_bounds__((NW + 1) * 32)
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
   constexpr int R = S::R;
@@ -200,6 +201,12 @@ __global__ void __launch_bounds__((NW + 1) * 32)
         a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
       acc[v] = a;
     }
+    if constexpr (PER) {
+      // periodic: the loaded ghost rows/cols hold valid wrap-around images, no ring
+#pragma unroll
+      for (int v = 0; v < V; ++v) res[v] = Ar::two(acc[v], minus[v]);
+      return;
+    }
     const int gi = p.row0 + row;
     const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
     if (row_in && cols_inner) {
@@ -257,6 +264,27 @@ __global__ void __launch_bounds__((NW + 1) * 32)
       for (int v = 0; v < V; ++v)
         if (gc0 + v < p.cols) dst[v] = res[v];
     }
+    if constexpr (PER) {
+      // refresh wrap-around images to depth D = R*TS (what the next pass loads)
+      const int D = R * TS;
+      const bool erow = (row < D) || (row >= p.rows - D);
+      const bool ecol = (gc0 < D) || (gc0 + V > p.cols - D);
+      if (erow || ecol) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int j = gc0 + v;
+          if (j >= p.cols) continue;
+          for (int a = -1; a <= 1; ++a)
+            for (int b = -1; b <= 1; ++b) {
+              if (a == 0 && b == 0) continue;
+              const int ii = row + a * p.rows;
+              const int jj = j + b * p.cols;
+              if (ii < -D || ii >= p.rows + D || jj < -D || jj >= p.cols + D) continue;
+              base[int64_t(ii) * pitch + jj] = res[v];
+            }
+        }
+      }
+    }
   };
 
   // One u^k row through every stage.  STEADY: all TS windows are full and the final row
@@ -307,7 +335,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     const T* su = s_uk + s * RB * LU;
     const T* sk = s_km + s * RB * LK;
     // whole strip away from the global ring and the right edge: no column masks
-    const bool cols_inner = (j0 - HT >= p.ring) && (j0 + W + HT <= p.cols - p.ring);
+    const bool cols_inner = PER || ((j0 - HT >= p.ring) && (j0 + W + HT <= p.cols - p.ring));
     const bool lane_store = lane_out && (j0 + gc_lane < p.cols);
     if (mlo >= 2 * R * TS && mlo + RB <= ne) {
 #pragma unroll

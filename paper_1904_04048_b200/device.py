@@ -45,12 +45,12 @@ class Simulation:
         radius = self.spec.radius
         self.ring = (radius if ring is None else int(ring)) if bc == "dirichlet" else 0
         self.rows = self.n + 1 if bc == "dirichlet" else self.n
-        self.grid = nat.make_grid(self.rows, self.rows, max(2, radius), self.ring, bc, dtype, arith)
         if tsteps not in (1, 2, 4):
             raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
-        if tsteps > 1 and bc != "dirichlet":
-            raise ValueError("temporal blocking supports Dirichlet grids only")
         self.tsteps = int(tsteps)
+        # periodic blocked passes read wrap-around images R*T deep
+        ghost = max(2, radius * tsteps) if bc == "periodic" else max(2, radius)
+        self.grid = nat.make_grid(self.rows, self.rows, ghost, self.ring, bc, dtype, arith)
         # temporal blocking writes two new levels while both inputs are still read: 4 levels
         self.levels = [nat.Level(self.grid) for _ in range(3 if tsteps == 1 else 4)]
         self.previous = None

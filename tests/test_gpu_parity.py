@@ -331,24 +331,32 @@ def test_config4_full_size_slab_check(oracle):
 @pytest.mark.parametrize("dtype,arith", [("f64", "ref"), ("f32", "ref"), ("f32", "native")])
 @pytest.mark.parametrize("tsteps", [2, 4])
 @pytest.mark.parametrize("n", [45, 700])
-def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps, n, oracle):
-    """T fused steps per pass equal T single steps bit for bit (incl. a remainder step)."""
+@pytest.mark.parametrize("bc", ["dirichlet", "periodic"])
+def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps, n, bc, oracle):
+    """T fused steps per pass equal T single steps bit for bit (incl. a remainder step,
+    then a second march call that starts blocked again)."""
     from paper_1904_04048_b200.device import Simulation
 
-    sim = Simulation(name, n, 0.4 if radius == 2 else 0.6, bc="dirichlet", dtype=dtype,
+    sim = Simulation(name, n, 0.4 if radius == 2 else 0.6, bc=bc, dtype=dtype,
                      arith=arith, tsteps=tsteps)
     rng = np.random.default_rng(7 * n + tsteps)
     npdt = np.float64 if dtype == "f64" else np.float32
     u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
     v0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    if bc == "periodic":
+        for f in (u0, v0):
+            f[:-1, -1] = f[:-1, 0]
+            f[-1, :] = f[0, :]
     sim.load_initial(u0, v0)
     sim.first_step()
     steps = 2 * tsteps + 1
     sim.march(steps)
+    sim.march(tsteps)
+    ring = radius if bc == "dirichlet" else 0
     o1 = oracle.first_step(u0, v0, pairs(sim.spec, "first_u", sim.lam),
-                           pairs(sim.spec, "first_v", sim.lam), sim.tau, "dirichlet", radius, arith)
-    want, want_prev = oracle.march(o1, u0, pairs(sim.spec, "two_step", sim.lam), steps,
-                                   "dirichlet", radius, arith)
+                           pairs(sim.spec, "first_v", sim.lam), sim.tau, bc, ring, arith)
+    want, want_prev = oracle.march(o1, u0, pairs(sim.spec, "two_step", sim.lam),
+                                   steps + tsteps, bc, ring, arith)
     assert same_bits(sim.field(), want)
     assert same_bits(sim.field("previous"), want_prev)
 
