@@ -34,7 +34,7 @@ CONFIGS = {
                steps=200, ic="gauss-centre",
                desc="C1: P5 5-point, 512^2 f64, Dirichlet ring 1, lambda=0.5, 200 steps"),
     "C2": dict(scheme="P9", n=4096, bc="periodic", ring=0, dtype="f64", arith="ref", lam=0.6,
-               steps=1000, ic="standing",
+               steps=1000, ic="standing", tb=4,
                desc="C2: P9 9-point, 4096^2 f64 periodic, lambda=0.6, standing wave m=4 n=6, 1000 steps"),
     "C3": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f64", arith="ref", lam=0.4,
                steps=500, ic=(32, 0.01, 0.05, False), tb=2,
@@ -295,7 +295,7 @@ def gpu_arm_single(args, cfg, cfg_name):
     import torch
 
     torch.cuda.set_device(torch.device("cuda", 0))
-    tb_ok = cfg["bc"] == "dirichlet"
+    tb_ok = True
     # auto: the fastest measured depth per config, 1 where blocking is n/a
     T = args.tsteps if args.tsteps > 0 else (cfg.get("tb", 1) if tb_ok else 1)
     companion = None
@@ -543,8 +543,8 @@ def main():
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
-                    help="temporal blocking depth; 0 = the config's measured best (C4: 4, "
-                         "C3/C5: 2, with an unblocked companion measurement; C1/C2: 1)")
+                    help="temporal blocking depth; 0 = the config's measured best (C2/C4: 4, "
+                         "C3/C5: 2, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

@@ -62,8 +62,11 @@ __device__ __forceinline__ T shfl_down1(T x) {
   return __shfl_down_sync(0xffffffffu, x, 1);
 }
 
+#ifndef PS_TB_MINB
+#define PS_TB_MINB 1  // tuning: minimum resident blocks per SM (caps registers per thread)
+#endif
 template <typename T, int A, class S, int TS, bool PER, int NW, int RB, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32)
+__global__ void __launch_bounds__((NW + 1) * 32, PS_TB_MINB)
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
   constexpr int R = S::R;
   using G = TBGeom<T, NW, RB, NS, R, TS>;
