@@ -210,6 +210,13 @@ ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, cons
                          double st, double* out2, void* stream);
 void ps_errsum_destroy(ps_errsum* e);
 
+/* Snapshot writer: one HOST rows x cols block as CSV, "%.17g" per
+ * value, "," between values, "\n" after each row — the text of the reference's
+ * dump_grid_csv (simulator.py:293-295, np.savetxt) byte for byte, without Python
+ * formatting cost.  Host-only; pair with an asynchronous ps_copy_out into pinned memory. */
+ps_status ps_write_csv(const char* path, const void* host, int64_t rows, int64_t cols,
+                       int64_t host_pitch, int32_t dtype);
+
 /* Kernel launches issued by this library since load (for launch accounting). */
 int64_t ps_launch_count(void);
 

@@ -54,6 +54,7 @@ EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_
            "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
+           "ps_write_csv",
            "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
@@ -97,6 +98,7 @@ def load_library(path: str = LIB_PATH):
             "ps_errsum_create": (vp, [i64, i64]),
             "ps_errsum_step": (i32, [vp, G, vp, vp, dbl, vp, vp]),
             "ps_errsum_destroy": (None, [vp]),
+            "ps_write_csv": (i32, [ctypes.c_char_p, vp, i64, i64, i64, i32]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
             "ps_version": (ctypes.c_char_p, []),
@@ -325,6 +327,18 @@ class ErrSum:
                 self._lib.ps_errsum_destroy(ctypes.c_void_p(h))
             except Exception:
                 pass
+
+
+def write_csv(path, values: np.ndarray):
+    """``%.17g`` CSV of a 2-D float64/float32 host array (dump_grid_csv's format)."""
+    arr = np.ascontiguousarray(values)
+    if arr.dtype not in (np.float64, np.float32) or arr.ndim != 2:
+        raise TypeError("write_csv takes a 2-D float64 or float32 array")
+    check(load_library().ps_write_csv(os.fsencode(str(path)),
+                                      arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                                      arr.shape[1], arr.shape[1],
+                                      DTYPE["f64" if arr.dtype == np.float64 else "f32"]),
+          "ps_write_csv")
 
 
 def launch_count() -> int:

@@ -1568,6 +1568,35 @@ ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, cons
   return last_cuda_status();
 }
 
+ps_status ps_write_csv(const char* path, const void* host, int64_t rows, int64_t cols,
+                       int64_t host_pitch, int32_t dtype) {
+  // Host-side writer for dump_grid_csv (simulator.py:293-295: np.savetxt(fmt="%.17g",
+  // delimiter=",")): one row per line, "%.17g" of each value widened to double.
+  if (!path || !host || rows < 0 || cols < 0 || host_pitch < cols) return PS_ERR_ARG;
+  if (dtype != PS_F64 && dtype != PS_F32) return PS_ERR_ARG;
+  FILE* f = std::fopen(path, "w");
+  if (!f) return PS_ERR_ARG;
+  std::vector<char> line;
+  line.reserve(size_t(cols) * 26 + 2);
+  char buf[40];
+  for (int64_t i = 0; i < rows; ++i) {
+    line.clear();
+    for (int64_t j = 0; j < cols; ++j) {
+      const double x = dtype == PS_F64 ? static_cast<const double*>(host)[i * host_pitch + j]
+                                       : double(static_cast<const float*>(host)[i * host_pitch + j]);
+      const int len = std::snprintf(buf, sizeof(buf), "%.17g", x);
+      if (j) line.push_back(',');
+      line.insert(line.end(), buf, buf + len);
+    }
+    line.push_back('\n');
+    if (std::fwrite(line.data(), 1, line.size(), f) != line.size()) {
+      std::fclose(f);
+      return PS_ERR_ARG;
+    }
+  }
+  return std::fclose(f) == 0 ? PS_OK : PS_ERR_ARG;
+}
+
 int64_t ps_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* ps_strerror(int32_t status) {

@@ -63,10 +63,21 @@ __device__ __forceinline__ T shfl_down1(T x) {
 }
 
 #ifndef PS_TB_MINB
-#define PS_TB_MINB 1  // tuning: minimum resident blocks per SM (caps registers per thread)
+#define PS_TB_MINB 0  // tuning override: minimum resident blocks per SM (caps registers)
 #endif
+// Measured (tools/): asking for 3 resident blocks (<= 136 registers) pays
+// for f32 at depth 2 (+2-4 %) and radius-1 f64 Dirichlet at depth 4 (+4 %); elsewhere
+// the extra spills cost more than the occupancy gains.
+template <typename T, class S, int TS, bool PER>
+constexpr int tb_minb() {
+  if (PS_TB_MINB > 0) return PS_TB_MINB;
+  if (sizeof(T) == 4 && TS == 2) return 3;
+  if (sizeof(T) == 8 && S::R == 1 && TS == 4 && !PER) return 3;
+  return 1;
+}
+
 template <typename T, int A, class S, int TS, bool PER, int NW, int RB, int NS>
-__global__ void __launch_bounds__((NW + 1) * 32, PS_TB_MINB)
+__global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
   constexpr int R = S::R;
   using G = TBGeom<T, NW, RB, NS, R, TS>;

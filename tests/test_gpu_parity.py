@@ -424,3 +424,27 @@ def test_dropin_tiny_grids_bitwise(ps, oracle, name, n):
         got = ps.two_step(a, b, spec, 0.5, bc)
         want = oracle.two_step(a, b, pairs(spec, "two_step", 0.5), bc, 1)
         assert same_bits(got, want), (name, n, bc)
+
+
+# ------------------------------------------------------------ snapshots / checkpoints (F3)
+def test_async_snapshot_and_checkpoint_resume(tmp_path):
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation("P9", 600, 0.6, bc="periodic", tsteps=2)
+    sim.gaussian_initial(8, 0.02, 0.08, seed=1)
+    sim.first_step()
+    sim.march(5)
+    th = sim.snapshot(tmp_path / "snap.csv")
+    want_snap = sim.field()
+    sim.march(6)                      # the march continues while the snapshot drains
+    th.join()
+    got = np.loadtxt(tmp_path / "snap.csv", delimiter=",")
+    assert same_bits(got, want_snap)
+    sim.save_checkpoint(tmp_path / "ck.npz")
+    sim.march(7)
+    final = sim.field()
+    other = Simulation("P9", 600, 0.6, bc="periodic", tsteps=2)
+    other.load_checkpoint(tmp_path / "ck.npz")
+    other.march(7)
+    assert same_bits(other.field(), final)
+    assert other.step == sim.step

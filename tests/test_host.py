@@ -257,3 +257,18 @@ def test_relative_l2_error_host():
     assert ps.relative_l2_error(fields, ps.exact_standing_wave, tau) == pytest.approx(1.0)
     with pytest.raises(ps.DegenerateNormError):
         ps.relative_l2_error([np.ones((5, 5))], lambda a, b, t: 0.0 * (a + b), 0.1)
+
+
+def test_csv_writer_matches_numpy_savetxt(tmp_path):
+    """F3: libps.so's %.17g writer produces np.savetxt's bytes (dump_grid_csv)."""
+    rng = np.random.default_rng(0)
+    for dt in (np.float64, np.float32):
+        a = (rng.standard_normal((7, 9)) * 10.0 ** rng.integers(-30, 30, (7, 9))).astype(dt)
+        a[0, 0], a[1, 1], a[2, 2], a[3, 3] = 0.0, -0.0, np.inf, np.nan
+        a[4, 4] = 1e-310 if dt == np.float64 else 1e-40
+        p1, p2 = tmp_path / "np.csv", tmp_path / "ps.csv"
+        np.savetxt(p1, a, delimiter=",", fmt="%.17g")
+        ps.dump_grid_csv(a, p2)
+        assert p1.read_bytes() == p2.read_bytes()
+    loaded = np.loadtxt(p2, delimiter=",")
+    assert loaded.shape == (7, 9)
