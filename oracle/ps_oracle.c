@@ -253,7 +253,7 @@ int ora_first_step(int dtype, int arith, int bc, int ring, int64_t rows, int64_t
         if (arith == ORA_NATIVE) {
           row_acc_f32nat(&tu, (const float*)u0, cols, per, n1, n2, ic, jlo, jhi, fu);
           row_acc_f32nat(&tv, (const float*)v0, cols, per, n1, n2, ic, jlo, jhi, fv);
-          for (int64_t j = jlo; j < jhi; ++j) o[j] = fmaf(tauf, fv[j - jlo], fu[j - jlo]);
+          for (int64_t j = jlo; j < jhi; ++j) o[j] = fu[j - jlo] + tauf * fv[j - jlo];
         } else {
           row_acc_f32ref(&tu, (const float*)u0, cols, per, n1, n2, ic, jlo, jhi, au);
           row_acc_f32ref(&tv, (const float*)v0, cols, per, n1, n2, ic, jlo, jhi, av);

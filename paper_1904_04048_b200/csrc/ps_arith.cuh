@@ -30,6 +30,11 @@ struct Arith<double, A> {
   __device__ __forceinline__ static double first(acc_t au, acc_t av, double tau) {
     return __dadd_rn(au, __dmul_rn(tau, av));
   }
+  // velocity half of the first step, negated: two(acc_u, vpart(acc_v)) == first(acc_u,
+  // acc_v) bit for bit, because a - (-b) = a + b exactly in IEEE arithmetic
+  __device__ __forceinline__ static double vpart(acc_t av, double tau) {
+    return -__dmul_rn(tau, av);
+  }
 };
 
 // f32, reference contract: numpy multiplies a float32 field by a Python float in
@@ -49,11 +54,14 @@ struct Arith<float, ARITH_REF> {
   __device__ __forceinline__ static float first(acc_t au, acc_t av, float tau) {
     return __fadd_rn(__double2float_rn(au), __fmul_rn(tau, __double2float_rn(av)));
   }
+  __device__ __forceinline__ static float vpart(acc_t av, float tau) {
+    return -__fmul_rn(tau, __double2float_rn(av));
+  }
 };
 
 // f32, native contract: the taps in the same table order, each folded in with one
 // correctly rounded fused multiply-add (acc = fma(c, u, acc) from +0.0), then a float32
-// subtract.  Half the floating-point instructions of the reference sequence and at
+// subtract (first step: acc_u + fl(tau * acc_v)).  Half the floating-point instructions of the reference sequence and at
 // least as accurate; checked bit for bit against the oracle's fmaf() chain and against
 // the f64 run within the stated tolerance.
 template <>
@@ -67,8 +75,12 @@ struct Arith<float, ARITH_NATIVE> {
   __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
     return __fsub_rn(acc, ukm1);
   }
+  // first step: acc_u + fl(tau * acc_v) (unfused, so it decomposes like the others)
   __device__ __forceinline__ static float first(acc_t au, acc_t av, float tau) {
-    return __fmaf_rn(tau, av, au);
+    return __fadd_rn(au, __fmul_rn(tau, av));
+  }
+  __device__ __forceinline__ static float vpart(acc_t av, float tau) {
+    return -__fmul_rn(tau, av);
   }
 };
 

@@ -127,6 +127,8 @@ struct StreamParams {
   // inconsistent alias, simulator.py:184); 0 = images of u^{k-1} are copies of its core
   // (every level the march produces), so the image value equals the core value
   int32_t img_exact;
+  double tau;              // VP launches: output -fl(tau * acc) (first step, velocity half)
+  float tauf;
   double c[PS_MAX_TAPS];
   float cf[PS_MAX_TAPS];
 };
@@ -147,7 +149,9 @@ constexpr int kSlots = 1024;
 __device__ unsigned int g_tile_next[kSlots];
 __device__ unsigned int g_tile_done[kSlots];
 
-template <typename T, int A, class S, bool PER, int NW, int RB, int NS>
+// VP = true: the first step's velocity half, -fl(tau * A_v(v0)), written where a second
+// (ordinary) launch with the displacement table reads it as "u^{k-1}"; no u^{k-1} loads.
+template <typename T, int A, class S, bool PER, int NW, int RB, int NS, bool VP = false>
 __global__ void __launch_bounds__((NW + 1) * 32)
     k_two_step_stream(const __grid_constant__ StreamParams p, const int slot) {
   using G = StreamGeom<T, NW, RB, NS>;
@@ -214,13 +218,13 @@ __global__ void __launch_bounds__((NW + 1) * 32)
           s_tile[s] = tid;
           s_mlo[s] = mlo;
           const int mhi = min(mlo + RB, ne);
-          const int nk = max(0, mhi - max(mlo, 2 * R));
+          const int nk = VP ? 0 : max(0, mhi - max(mlo, 2 * R));
           mbar_arrive_expect_tx(&full[s], uint32_t(mhi - mlo) * ukb + uint32_t(nk) * kmb);
           for (int m = mlo; m < mhi; ++m) {
             const int64_t e = int64_t(i0) - R + m;
             tma_load_1d(s_uk + (s * RB + (m - mlo)) * SU, uk + e * pitch + j0 - V, ukb, &full[s],
                         pol_uk);
-            if (m >= 2 * R) {
+            if (!VP && m >= 2 * R) {
               const int64_t i = int64_t(i0) + m - 2 * R;
               tma_load_1d(s_km + (s * RB + (m - mlo)) * W, ukm1 + i * pitch + j0, kmb, &full[s],
                           pol_km);
@@ -279,9 +283,19 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     if (m < 2 * R || !active) return;
     const int i = i0 + m - 2 * R;
     T km[V];
-    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + tcol), km);
+    if constexpr (!VP) Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + tcol), km);
     acc_t acc[V];
     T out[V];
+    auto fin = [&](acc_t a, T kmv) -> T {
+      if constexpr (VP) {
+        if constexpr (sizeof(T) == sizeof(double))
+          return Ar::vpart(a, p.tau);
+        else
+          return Ar::vpart(a, p.tauf);
+      } else {
+        return Ar::two(a, kmv);
+      }
+    };
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       acc_t a = Ar::zero();
@@ -292,19 +306,19 @@ __global__ void __launch_bounds__((NW + 1) * 32)
     T* dst = ukp1 + int64_t(i) * pitch + jv;
     if constexpr (PER) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) out[v] = Ar::two(acc[v], km[v]);
+      for (int v = 0; v < V; ++v) out[v] = fin(acc[v], km[v]);
     } else {
       const int gi = p.row0 + i;
       const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
       if (row_in && cols_inner) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) out[v] = Ar::two(acc[v], km[v]);
+        for (int v = 0; v < V; ++v) out[v] = fin(acc[v], km[v]);
       } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const int j = jv + v;
           const bool in = row_in && (j >= p.ring) && (j < p.cols - p.ring);
-          out[v] = in ? Ar::two(acc[v], km[v]) : T(0);
+          out[v] = in ? fin(acc[v], km[v]) : T(0);
         }
       }
     }
@@ -347,7 +361,7 @@ __global__ void __launch_bounds__((NW + 1) * 32)
               const int jj = j + b * p.cols;
               if (ii < -R || ii >= p.rows + R || jj < -R || jj >= p.cols + R) continue;
               const int64_t o = int64_t(ii) * pitch + jj;
-              ukp1[o] = p.img_exact ? Ar::two(acc[v], ukm1[o]) : out[v];
+              ukp1[o] = (!VP && p.img_exact) ? Ar::two(acc[v], ukm1[o]) : out[v];
             }
         }
       }
@@ -698,15 +712,15 @@ static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, 
   return last_cuda_status();
 }
 
-template <typename T, int A, class S, bool PER>
+template <typename T, int A, class S, bool PER, bool VP = false>
 static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
                                const ps_table* t, int64_t rlo, int64_t rhi, cudaStream_t st,
-                               const Halo& h) {
+                               const Halo& h, double tau = 0.0) {
   constexpr int NW = PS_NW;
   constexpr int RB = (S::R == 1) ? PS_RB1 : PS_RB2;
   constexpr int NS = PS_NS;
   using Gm = StreamGeom<T, NW, RB, NS>;
-  auto kern = k_two_step_stream<T, A, S, PER, NW, RB, NS>;
+  auto kern = k_two_step_stream<T, A, S, PER, NW, RB, NS, VP>;
   static std::once_flag once;
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {
@@ -734,6 +748,8 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   p.up_rows = h.up_rows;
   p.img_exact = h.img_consistent ? 0 : 1;
   p.reverse = h.reverse ? 1 : 0;
+  p.tau = tau;
+  p.tauf = static_cast<float>(tau);
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -1036,6 +1052,37 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
   return exec;
 }
 
+// First step as two streaming launches: u1 <- -fl(tau * A_v(v0)) (VP), then the ordinary
+// two-step kernel u1 <- fl(A_u(u0) - u1) = fl(A_u(u0) + fl(tau * A_v(v0))), bit for bit the
+// reference's first step.  Both tables must have a specialised shape.
+template <typename T, int A, bool PER>
+static ps_status first_step_stream(const ps_grid* g, const void* u0, const void* v0, void* u1,
+                                   const ps_table* tu, const ps_table* tv, double tau,
+                                   cudaStream_t st, bool* done) {
+  *done = true;
+  const Halo h;
+  ps_status s;
+  if (shape_matches<ShapeP5>(tv))
+    s = launch_stream<T, A, ShapeP5, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeP9>(tv))
+    s = launch_stream<T, A, ShapeP9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeC9>(tv))
+    s = launch_stream<T, A, ShapeC9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeP13>(tv))
+    s = launch_stream<T, A, ShapeP13, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else {
+    *done = false;
+    return PS_OK;
+  }
+  if (s != PS_OK) return s;
+  return dispatch_two_step<T, A, PER>(g, u0, u1, u1, tu, 0, g->rows, st, h);
+}
+
+static bool stream_shape(const ps_table* t) {
+  return shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) || shape_matches<ShapeC9>(t) ||
+         shape_matches<ShapeP13>(t);
+}
+
 }  // namespace ps
 
 // ===========================================================================
@@ -1178,6 +1225,21 @@ ps_status ps_first_step(const ps_grid* g, const void* u0, const void* v0, void* 
   if (!aligned16(u0) || !aligned16(v0) || !aligned16(u1)) return PS_ERR_ALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool per = g->bc == PS_BC_PERIODIC;
+  if (u1 != u0 && u1 != v0 && stream_shape(tu) && stream_shape(tv) && g->rows >= 4 &&
+      g->cols >= 4 && env_int("PS_FORCE_GENERIC", 0) == 0) {
+    bool done = false;
+    if (g->dtype == PS_F64)
+      s = per ? first_step_stream<double, ARITH_REF, true>(g, u0, v0, u1, tu, tv, tau, st, &done)
+              : first_step_stream<double, ARITH_REF, false>(g, u0, v0, u1, tu, tv, tau, st, &done);
+    else if (g->arith == PS_ARITH_NATIVE)
+      s = per ? first_step_stream<float, ARITH_NATIVE, true>(g, u0, v0, u1, tu, tv, tau, st, &done)
+              : first_step_stream<float, ARITH_NATIVE, false>(g, u0, v0, u1, tu, tv, tau, st,
+                                                              &done);
+    else
+      s = per ? first_step_stream<float, ARITH_REF, true>(g, u0, v0, u1, tu, tv, tau, st, &done)
+              : first_step_stream<float, ARITH_REF, false>(g, u0, v0, u1, tu, tv, tau, st, &done);
+    if (done || s != PS_OK) return s;
+  }
   if (g->dtype == PS_F64)
     return per ? launch_generic<double, ARITH_REF, true, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st)
                : launch_generic<double, ARITH_REF, false, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st);

@@ -448,3 +448,81 @@ def test_async_snapshot_and_checkpoint_resume(tmp_path):
     other.march(7)
     assert same_bits(other.field(), final)
     assert other.step == sim.step
+
+
+# ------------------------------------------------------------ full-size BASELINE properties
+def _checksum(level):
+    """Exact, order-independent checksum of a level's logical block: the sum of its
+    bit patterns as 64-bit integers (equal checksums <=> equal bits, w.h.p.)."""
+    import torch
+
+    v = level.view()
+    bits = v.view(torch.int64) if v.dtype == torch.float64 else v.view(torch.int32)
+    return int(bits.to(torch.int64).sum().item())
+
+
+def test_config5_full_size_blocking_is_bitwise():
+    """C5 (P13, ring 2, 65536^2 f32 native, 128 Gaussians): T=2 and T=4 marches give the
+    T=1 march's bits after 8 steps (checksums of both live levels)."""
+    import torch
+
+    from paper_1904_04048_b200.device import Simulation
+
+    sums = {}
+    for ts in (1, 2, 4):
+        sim = Simulation("P13", 65535, 0.4, bc="dirichlet", dtype="f32", arith="native",
+                         tsteps=ts)
+        sim.gaussian_initial(128, 0.002, 0.01, seed=0)
+        sim.first_step()
+        sim.march(8)
+        sums[ts] = (_checksum(sim.levels[sim.newest]), _checksum(sim.levels[sim.previous]))
+        del sim
+        torch.cuda.empty_cache()
+    assert sums[2] == sums[1] and sums[4] == sums[1], sums
+
+
+def test_config5_full_size_f32_against_f64():
+    """C5's stated check at full size: the f32 run against an f64 run on the same seed
+    after 100 steps, relative max-norm <= 2 n_t^2 2^-24."""
+    import torch
+
+    from paper_1904_04048_b200.device import Simulation
+
+    # 3 f64 levels (103 GB) + the kept copy (34 GB) fit one B200; blocking would need 4
+    sim = Simulation("P13", 65535, 0.4, bc="dirichlet", dtype="f64", tsteps=1)
+    sim.gaussian_initial(128, 0.002, 0.01, seed=0)
+    sim.first_step()
+    sim.march(99)
+    ref = sim.levels[sim.newest].view().clone()
+    del sim
+    torch.cuda.empty_cache()
+    sim = Simulation("P13", 65535, 0.4, bc="dirichlet", dtype="f32", arith="native", tsteps=2)
+    sim.gaussian_initial(128, 0.002, 0.01, seed=0)
+    sim.first_step()
+    sim.march(99)
+    got = sim.levels[sim.newest].view()
+    scale = ref.abs().max().item()
+    diff = 0.0
+    for r0 in range(0, ref.shape[0], 4096):   # chunked: no 34 GB temporaries
+        d = (got[r0:r0 + 4096].to(torch.float64) - ref[r0:r0 + 4096]).abs().max().item()
+        diff = max(diff, d)
+    rel = diff / scale
+    assert rel <= 2 * 100**2 * 2.0**-24, rel
+
+
+def test_config3_full_size_slab_check(oracle):
+    """C3 at full size (P13, ring 2, 16384^2 f64, 32 Gaussians): one step over a band of
+    rows checked bitwise against the oracle on the downloaded neighbourhood."""
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation("P13", 16383, 0.4, bc="dirichlet")
+    sim.gaussian_initial(32, 0.01, 0.05, seed=0)
+    sim.first_step()
+    sim.march(4)
+    band = slice(8190 - 2, 8230 + 2)
+    uk = sim.levels[sim.newest].view()[band].cpu().numpy()
+    ukm1 = sim.levels[sim.previous].view()[band].cpu().numpy()
+    sim.march(1)
+    got = sim.levels[sim.newest].view()[8190:8230].cpu().numpy()
+    want = oracle.two_step(uk, ukm1, pairs(sim.spec, "two_step", 0.4), "dirichlet", 2)[2:-2]
+    assert same_bits(got, want)
