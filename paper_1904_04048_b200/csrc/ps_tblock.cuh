@@ -204,7 +204,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
 
   const int gc_lane = warp * WO + lane * V - HT;  // own column relative to the strip start
 
-  auto stage_out = [&](int t, const T* minus, int row, int gc0, bool cols_inner, T* res) {
+  auto stage_out = [&](auto interior_tag, int t, const T* minus, int row, int gc0,
+                       bool cols_inner, T* res) {
+    constexpr bool INTERIOR = decltype(interior_tag)::value;
     // level k+t+1 at `row` from window t; minus = level k+t-1 at the same row
     acc_t acc[V];
 #pragma unroll
@@ -215,8 +217,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
         a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
       acc[v] = a;
     }
-    if constexpr (PER) {
-      // periodic: the loaded ghost rows/cols hold valid wrap-around images, no ring
+    if constexpr (PER || INTERIOR) {
+      // periodic (ghosts hold valid images) or a slot whose rows and strip are all off
+      // the Dirichlet ring: nothing to mask
 #pragma unroll
       for (int v = 0; v < V; ++v) res[v] = Ar::two(acc[v], minus[v]);
       return;
@@ -304,8 +307,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
   // One u^k row through every stage.  STEADY: all TS windows are full and the final row
   // lies inside the tile (no per-stage checks, so the unrolled window rotation compiles
   // to register renaming).  Otherwise stage t+1 runs only once window t is full.
-  auto row_step = [&](auto steady_tag, const T* su_row, const T* sk_row, int m, int i0, int i1,
-                      int j0, bool cols_inner, bool lane_store) {
+  auto row_step = [&](auto steady_tag, auto interior_tag, const T* su_row, const T* sk_row,
+                      int m, int i0, int i1, int j0, bool cols_inner, bool lane_store) {
     constexpr bool STEADY = decltype(steady_tag)::value;
     admit_uk(su_row);
     const int e = i0 - R * TS + m;
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
         for (int v = 0; v < V; ++v) minus[v] = win[t - 1][0][R + v];
       }
       T res[V];
-      stage_out(t, minus, row, gc0, cols_inner, res);
+      stage_out(interior_tag, t, minus, row, gc0, cols_inner, res);
       if (t == TS - 1) {
         if (lane_store && (STEADY || (row >= i0 && row < i1))) store_vec(out_last, row, gc0, res);
       } else {
@@ -351,16 +354,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     // whole strip away from the global ring and the right edge: no column masks
     const bool cols_inner = PER || ((j0 - HT >= p.ring) && (j0 + W + HT <= p.cols - p.ring));
     const bool lane_store = lane_out && (j0 + gc_lane < p.cols);
-    if (mlo >= 2 * R * TS && mlo + RB <= ne) {
+    const bool steady = mlo >= 2 * R * TS && mlo + RB <= ne;
+    // every stage output row of this slot lies in [row0+rmin, row0+rmax]
+    const int rmin = i0 - R * TS + mlo - TS * R, rmax = i0 - R * TS + mlo + RB - 1 - R;
+    const bool interior = cols_inner && (p.row0 + rmin >= p.ring) &&
+                          (p.row0 + rmax < p.grows - p.ring);
+    if (steady && interior) {
 #pragma unroll
       for (int mm = 0; mm < RB; ++mm)
-        row_step(std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner,
-                 lane_store);
+        row_step(std::true_type{}, std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
+                 j0, cols_inner, lane_store);
+    } else if (steady) {
+#pragma unroll
+      for (int mm = 0; mm < RB; ++mm)
+        row_step(std::true_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0,
+                 i1, j0, cols_inner, lane_store);
     } else {
 #pragma unroll 1
       for (int mm = 0; mm < min(RB, ne - mlo); ++mm)
-        row_step(std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner,
-                 lane_store);
+        row_step(std::false_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0,
+                 i1, j0, cols_inner, lane_store);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
