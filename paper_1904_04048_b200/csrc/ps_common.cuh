@@ -1,0 +1,461 @@
+// ps_common.cuh — everything the kernel translation units share: the per-point
+// contracts, the kernels (templates), host helpers, launchers and shape dispatch.
+// ps_device.cu holds the C-ABI; ps_kern_{f64,f32r,f32n}.cu instantiate the streaming,
+// temporal-blocking and first-step kernels for one (dtype, contract) each, so the three
+// compile in parallel.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "ps.h"
+#include "ps_arith.cuh"
+#include "ps_ptx.cuh"
+
+// Streaming-kernel geometry (tuning builds override with -D): consumer warps per
+// block, rows per pipeline stage for radius 1 / radius 2, pipeline stages.
+#ifndef PS_NW
+#define PS_NW 8
+#endif
+#ifndef PS_RB1
+#define PS_RB1 4
+#endif
+#ifndef PS_RB2
+#define PS_RB2 4
+#endif
+#ifndef PS_NS
+#define PS_NS 3
+#endif
+
+namespace ps {
+
+// launch accounting / per-launch tile-counter slots (defined in ps_device.cu)
+extern std::atomic<int64_t> g_launches;
+extern std::atomic<uint64_t> g_launch_seq;
+
+#include "ps_stream.cuh"
+
+#include "ps_tblock.cuh"
+
+#include "ps_generic.cuh"
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+struct DevInfo {
+  int nsm = 0;
+};
+inline DevInfo dev_info() {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev].nsm == 0) cudaDeviceGetAttribute(&cache[dev].nsm, cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* s = std::getenv(name);
+  return (s && *s) ? std::atoi(s) : dflt;
+}
+
+static ps_status last_cuda_status() {
+  return cudaGetLastError() == cudaSuccess ? PS_OK : PS_ERR_CUDA;
+}
+
+// Launch with programmatic stream serialization (PDL) unless PS_PDL=0: the kernel's
+// blocks may be scheduled while the previous kernel in the stream drains; the kernel
+// itself waits (griddepcontrol.wait) before reading anything the predecessor wrote.
+template <typename Params>
+static cudaError_t launch_pdl(void (*kern)(Params, int), int grid, int block, size_t smem,
+                              cudaStream_t st, const Params& p, int slot) {
+  static const bool pdl = env_int("PS_PDL", 1) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, p, slot);
+}
+
+template <typename T>
+static T* at_origin(const ps_grid* g, const void* level) {
+  return static_cast<T*>(const_cast<void*>(level)) + g->origin;
+}
+
+static int table_radius(const ps_table* t) {
+  int r = 0;
+  for (int s = 0; s < t->ntaps; ++s) r = std::max(r, std::max(std::abs(t->q1[s]), std::abs(t->q2[s])));
+  return r;
+}
+
+inline ps_status check_table(const ps_grid* g, const ps_table* t) {
+  if (!t || t->ntaps < 1 || t->ntaps > PS_MAX_TAPS) return PS_ERR_TABLE;
+  const int r = table_radius(t);
+  if (r > g->ghost) return PS_ERR_TABLE;
+  if (g->bc == PS_BC_DIRICHLET && r > g->ring) return PS_ERR_RADIUS;
+  return PS_OK;
+}
+
+inline ps_status check_grid(const ps_grid* g) {
+  if (!g) return PS_ERR_ARG;
+  if (g->bc != PS_BC_DIRICHLET && g->bc != PS_BC_PERIODIC) return PS_ERR_ARG;
+  if (g->dtype != PS_F64 && g->dtype != PS_F32) return PS_ERR_ARG;
+  if (g->arith != PS_ARITH_REF && g->arith != PS_ARITH_NATIVE) return PS_ERR_ARG;
+  if (g->rows < 1 || g->cols < 1 || g->rows > (1LL << 30) || g->cols > (1LL << 30))
+    return PS_ERR_SHAPE;
+  if (g->row0 < 0 || g->row0 + g->rows > g->grows) return PS_ERR_SHAPE;
+  return PS_OK;
+}
+
+static void fill_gen_table(GenTable& d, const ps_table* t) {
+  std::memset(&d, 0, sizeof(d));
+  if (!t) return;
+  d.ntaps = t->ntaps;
+  for (int s = 0; s < t->ntaps; ++s) {
+    d.q1[s] = t->q1[s];
+    d.q2[s] = t->q2[s];
+    d.c[s] = t->c[s];
+    d.cf[s] = static_cast<float>(t->c[s]);
+  }
+}
+
+static dim3 gen_grid(int64_t rows, int64_t cols) {
+  const int nsm = std::max(1, dev_info().nsm);
+  int64_t gx = (cols + 31) / 32;
+  int64_t gy = (rows + 7) / 8;
+  gx = std::min<int64_t>(gx, 1024);
+  gy = std::min<int64_t>(gy, std::max<int64_t>(1, int64_t(nsm) * 64 / gx + 1));
+  gy = std::min<int64_t>(gy, 65535);
+  return dim3(unsigned(gx), unsigned(gy));
+}
+
+static bool single_slab(const ps_grid* g) { return g->row0 == 0 && g->grows == g->rows; }
+
+// Peer halo targets of a row-slab update (logical-origin pointers of the neighbours'
+// u^{k+1} levels; null = no neighbour / exchange done elsewhere).
+struct Halo {
+  void* up = nullptr;
+  void* dn = nullptr;
+  int32_t up_rows = 0;
+  bool img_consistent = false;  // periodic input images are copies of the core (march)
+  bool reverse = false;         // walk tiles bottom-up
+};
+
+template <typename T, int A, bool PER, bool FIRST>
+static ps_status launch_generic(const ps_grid* g, const void* a, const void* b, void* out,
+                                const ps_table* ta, const ps_table* tb, double tau,
+                                int64_t rlo, int64_t rhi, cudaStream_t st,
+                                const Halo& h = Halo{}) {
+  GenParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.a = at_origin<T>(g, a);
+  p.b = at_origin<T>(g, b);
+  p.out = at_origin<T>(g, out);
+  p.pitch = g->pitch;
+  p.rows = int32_t(g->rows);
+  p.cols = int32_t(g->cols);
+  p.ring = PER ? 0 : g->ring;
+  p.radius = std::max(table_radius(ta), tb ? table_radius(tb) : 0);
+  p.row0 = int32_t(g->row0);
+  p.grows = int32_t(g->grows);
+  p.rlo = int32_t(rlo);
+  p.rhi = int32_t(rhi);
+  p.row_images = (PER && single_slab(g)) ? 1 : 0;
+  p.halo_up = h.up;
+  p.halo_dn = h.dn;
+  p.up_rows = h.up_rows;
+  p.tau = tau;
+  p.tauf = static_cast<float>(tau);
+  fill_gen_table(p.ta, ta);
+  fill_gen_table(p.tb, tb);
+  if (rhi <= rlo) return PS_OK;
+  k_generic<T, A, PER, FIRST><<<gen_grid(rhi - rlo, g->cols), dim3(32, 8), 0, st>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return last_cuda_status();
+}
+
+template <typename T, int A, class S, bool PER, bool VP = false>
+static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                               const ps_table* t, int64_t rlo, int64_t rhi, cudaStream_t st,
+                               const Halo& h, double tau = 0.0) {
+  constexpr int NW = PS_NW;
+  constexpr int RB = (S::R == 1) ? PS_RB1 : PS_RB2;
+  constexpr int NS = PS_NS;
+  using Gm = StreamGeom<T, NW, RB, NS>;
+  auto kern = k_two_step_stream<T, A, S, PER, NW, RB, NS, VP>;
+  static std::once_flag once;
+  static int blocks_per_sm = 1;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, (NW + 1) * 32,
+                                                  Gm::smem_bytes);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  });
+  StreamParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.uk = at_origin<T>(g, uk);
+  p.ukm1 = at_origin<T>(g, ukm1);
+  p.ukp1 = at_origin<T>(g, ukp1);
+  p.pitch = g->pitch;
+  p.rows = int32_t(g->rows);
+  p.cols = int32_t(g->cols);
+  p.ring = PER ? 0 : g->ring;
+  p.row0 = int32_t(g->row0);
+  p.grows = int32_t(g->grows);
+  p.rlo = int32_t(rlo);
+  p.rhi = int32_t(rhi);
+  p.row_images = (PER && single_slab(g)) ? 1 : 0;
+  p.halo_up = h.up;
+  p.halo_dn = h.dn;
+  p.up_rows = h.up_rows;
+  p.img_exact = h.img_consistent ? 0 : 1;
+  p.reverse = h.reverse ? 1 : 0;
+  p.tau = tau;
+  p.tauf = static_cast<float>(tau);
+  for (int s = 0; s < S::N; ++s) {
+    p.c[s] = t->c[s];
+    p.cf[s] = static_cast<float>(t->c[s]);
+  }
+  const int64_t nrows = rhi - rlo;
+  if (nrows <= 0) return PS_OK;
+  const int resident = std::max(1, dev_info().nsm) * blocks_per_sm;
+  p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
+  int rc = env_int("PS_ROW_CHUNK", 0);
+  if (rc <= 0) {
+    // Tiles are claimed dynamically, so balance only needs ~8 tiles per resident block;
+    // taller tiles re-read fewer halo rows (2R per tile).  128 rows keeps the tail
+    // under one ~25 us tile on the big grids; medium grids drop to >= 16 rows.
+    const int64_t want_tiles = int64_t(resident) * 8;
+    const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
+    rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
+    rc = std::max(rc, std::max(16, 8 * S::R));
+    rc = std::min(rc, 128);
+    // small grids (L2-resident, latency-bound): more, shorter tiles beat fewer halo rows
+    if (p.nstrips * ((nrows + rc - 1) / rc) < resident) rc = std::max(4, 2 * S::R);
+  }
+  rc = int(std::min<int64_t>(rc, nrows));
+  p.rc = rc;
+  const int64_t nchunks = (nrows + rc - 1) / rc;
+  p.ntiles = int32_t(nchunks * p.nstrips);
+  const int grid = int(std::min<int64_t>(p.ntiles, resident));
+  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
+    return PS_ERR_CUDA;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return last_cuda_status();
+}
+
+template <typename T, int A, bool PER>
+static ps_status dispatch_two_step(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
+                                   const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,
+                                   const Halo& h) {
+  // The streaming kernel wants >= 4 rows/cols and at least one wrap (n >= R) for images.
+  const bool small = g->rows < 4 || g->cols < 4;
+  if (!small && env_int("PS_FORCE_GENERIC", 0) == 0) {
+    if (shape_matches<ShapeP5>(t))
+      return launch_stream<T, A, ShapeP5, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+    if (shape_matches<ShapeP9>(t))
+      return launch_stream<T, A, ShapeP9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+    if (shape_matches<ShapeC9>(t))
+      return launch_stream<T, A, ShapeC9, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+    if (shape_matches<ShapeP13>(t))
+      return launch_stream<T, A, ShapeP13, PER>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+  }
+  return launch_generic<T, A, PER, false>(g, uk, ukm1, ukp1, t, nullptr, 0.0, lo, hi, st, h);
+}
+
+template <typename T, int A>
+static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const void* ukm1,
+                                      void* ukp1, const ps_table* t, int64_t lo, int64_t hi,
+                                      cudaStream_t st, const Halo& h) {
+  if (g->bc == PS_BC_PERIODIC)
+    return dispatch_two_step<T, A, true>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+  return dispatch_two_step<T, A, false>(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+}
+
+// ---------------------------------------------------------------------------
+// Temporal blocking (ps_tblock.cuh)
+// ---------------------------------------------------------------------------
+// Geometry (measured on B200, profiles/ and DESIGN.md): 4 consumer warps x 3 stages,
+// except f32 at depth 4, whose ~224-register windows allow one block per SM — there 8
+// warps x 2 stages keep more warps resident.  Tuning builds override with -D.
+#ifndef PS_TB_NW
+#define PS_TB_NW 0
+#endif
+#ifndef PS_TB_RB
+#define PS_TB_RB 0  // 0: 2R+1 rows per stage, so a stage is one full window rotation
+#endif
+#ifndef PS_TB_NS
+#define PS_TB_NS 0
+#endif
+template <typename T, int TS>
+constexpr int tb_nw() {
+  return PS_TB_NW > 0 ? PS_TB_NW : ((TS == 4 && sizeof(T) == 4) ? 8 : 4);
+}
+template <typename T, int TS>
+constexpr int tb_ns() {
+  return PS_TB_NS > 0 ? PS_TB_NS : ((TS == 4 && sizeof(T) == 4) ? 2 : 3);
+}
+
+template <typename T, int A, class S, int TS, bool PER>
+static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
+                           void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
+                           cudaStream_t st, bool reverse) {
+  constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
+  using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
+  auto kern = k_two_step_tb<T, A, S, TS, PER, NW, RB, NS>;
+  static std::once_flag once;
+  static int blocks_per_sm = 1;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, (NW + 1) * 32,
+                                                  Gm::smem_bytes);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  });
+  const int64_t nrows = rhi - rlo;
+  if (nrows <= 0) return PS_OK;
+  TBParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.uk = at_origin<T>(g, uk);
+  p.ukm1 = at_origin<T>(g, ukm1);
+  p.out_prev = at_origin<T>(g, out_prev);
+  p.out_last = at_origin<T>(g, out_last);
+  p.pitch = g->pitch;
+  p.rows = int32_t(g->rows);
+  p.cols = int32_t(g->cols);
+  p.ring = PER ? 0 : g->ring;
+  p.row0 = int32_t(g->row0);
+  p.grows = int32_t(g->grows);
+  p.rlo = int32_t(rlo);
+  p.rhi = int32_t(rhi);
+  p.gmin = -int32_t(g->ghost);
+  p.gmax = int32_t(g->rows + g->ghost);
+  p.cmax = int32_t(g->pitch - (g->origin - g->ghost * g->pitch));
+  p.reverse = reverse ? 1 : 0;
+  for (int s = 0; s < S::N; ++s) {
+    p.c[s] = t->c[s];
+    p.cf[s] = static_cast<float>(t->c[s]);
+  }
+  const int resident = std::max(1, dev_info().nsm) * blocks_per_sm;
+  p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
+  int rc = env_int("PS_TB_ROW_CHUNK", 0);
+  if (rc <= 0) {
+    const int64_t want_tiles = int64_t(resident) * 8;
+    const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
+    rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
+    rc = std::max(rc, std::max(32, 8 * S::R * TS));
+    rc = std::min(rc, 256);
+  }
+  rc = int(std::min<int64_t>(rc, nrows));
+  p.rc = rc;
+  p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
+  const int grid = int(std::min<int64_t>(p.ntiles, resident));
+  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
+    return PS_ERR_CUDA;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return last_cuda_status();
+}
+
+template <typename T, int A, int TS>
+static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
+                             void* ol, const ps_table* t, int64_t lo, int64_t hi,
+                             cudaStream_t st, bool rev) {
+  if (shape_matches<ShapeP5>(t))
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+  if (shape_matches<ShapeP9>(t))
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+  if (shape_matches<ShapeC9>(t))
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+  if (shape_matches<ShapeP13>(t))
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+  return PS_ERR_TABLE;
+}
+
+// First step as two streaming launches: u1 <- -fl(tau * A_v(v0)) (VP), then the ordinary
+// two-step kernel u1 <- fl(A_u(u0) - u1) = fl(A_u(u0) + fl(tau * A_v(v0))), bit for bit the
+// reference's first step.  Both tables must have a specialised shape.
+template <typename T, int A, bool PER>
+static ps_status first_step_stream(const ps_grid* g, const void* u0, const void* v0, void* u1,
+                                   const ps_table* tu, const ps_table* tv, double tau,
+                                   cudaStream_t st, bool* done) {
+  *done = true;
+  const Halo h;
+  ps_status s;
+  if (shape_matches<ShapeP5>(tv))
+    s = launch_stream<T, A, ShapeP5, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeP9>(tv))
+    s = launch_stream<T, A, ShapeP9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeC9>(tv))
+    s = launch_stream<T, A, ShapeC9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else if (shape_matches<ShapeP13>(tv))
+    s = launch_stream<T, A, ShapeP13, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+  else {
+    *done = false;
+    return PS_OK;
+  }
+  if (s != PS_OK) return s;
+  return dispatch_two_step<T, A, PER>(g, u0, u1, u1, tu, 0, g->rows, st, h);
+}
+
+
+// ---------------------------------------------------------------------------
+// Typed entry points, one translation unit per (dtype, contract): ps_kern_*.cu
+// ---------------------------------------------------------------------------
+#define PS_TYPED_DECL(SFX)                                                                  \
+  ps_status two_step_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,  \
+                           const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,      \
+                           const Halo& h);                                                  \
+  ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
+                     const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
+                     bool rev);                                                             \
+  ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
+                        const ps_table* tu, const ps_table* tv, double tau, cudaStream_t st, \
+                        bool* done);
+PS_TYPED_DECL(f64)
+PS_TYPED_DECL(f32r)
+PS_TYPED_DECL(f32n)
+#undef PS_TYPED_DECL
+
+#define PS_TYPED_DEFINE(SFX, T, A)                                                          \
+  ps_status two_step_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,  \
+                           const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,      \
+                           const Halo& h) {                                                 \
+    return dispatch_two_step_bc<T, A>(g, uk, ukm1, ukp1, t, lo, hi, st, h);                 \
+  }                                                                                         \
+  ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
+                     const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
+                     bool rev) {                                                            \
+    switch (tsteps) {                                                                       \
+      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);         \
+      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);         \
+      default: return PS_ERR_ARG;                                                           \
+    }                                                                                       \
+  }                                                                                         \
+  ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
+                        const ps_table* tu, const ps_table* tv, double tau, cudaStream_t st, \
+                        bool* done) {                                                       \
+    return g->bc == PS_BC_PERIODIC                                                          \
+               ? first_step_stream<T, A, true>(g, u0, v0, u1, tu, tv, tau, st, done)        \
+               : first_step_stream<T, A, false>(g, u0, v0, u1, tu, tv, tau, st, done);      \
+  }
+
+}  // namespace ps
