@@ -526,3 +526,24 @@ def test_config3_full_size_slab_check(oracle):
     got = sim.levels[sim.newest].view()[8190:8230].cpu().numpy()
     want = oracle.two_step(uk, ukm1, pairs(sim.spec, "two_step", 0.4), "dirichlet", 2)[2:-2]
     assert same_bits(got, want)
+
+
+def test_dropin_is_thread_safe(ps, oracle):
+    """The reference's functions are safe from concurrent threads (README.md:111-112);
+    so are the drop-in's (per-thread device workspaces, stream-ordered C-ABI)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    spec = ps.named_scheme("P9")
+    rng = np.random.default_rng(21)
+    jobs = [(rng.normal(size=(n + 1, n + 1)), rng.normal(size=(n + 1, n + 1)), bc)
+            for n in (64, 200, 513, 64, 200, 513, 300, 301) for bc in ("dirichlet", "periodic")]
+
+    def work(job):
+        a, b, bc = job
+        return ps.two_step(a, b, spec, 0.6, bc)
+
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        results = list(pool.map(work, jobs))
+    for (a, b, bc), got in zip(jobs, results):
+        want = oracle.two_step(a, b, pairs(spec, "two_step", 0.6), bc, 1)
+        assert same_bits(got, want)
