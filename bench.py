@@ -46,7 +46,7 @@ CONFIGS = {
                steps=200, ic=(64, 0.01, 0.05, True), tb=4,
                desc="C4: P9 9-point, 32768^2 f64, Dirichlet ring 1, lambda=0.6, 200 steps"),
     "C5": dict(scheme="P13", n=65535, bc="dirichlet", ring=2, dtype="f32", arith="native",
-               lam=0.4, steps=100, ic=(128, 0.002, 0.01, False), tb=2,
+               lam=0.4, steps=100, ic=(128, 0.002, 0.01, False), tb=4,
                desc="C5: P13 13-point, 65536^2 f32, Dirichlet ring 2, lambda=0.4, 100 steps"),
 }
 
@@ -543,8 +543,8 @@ def main():
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
-                    help="temporal blocking depth; 0 = the config's measured best (C2/C4: 4, "
-                         "C3/C5: 2, with an unblocked companion measurement; C1: 1)")
+                    help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5: "
+                         "4, C3: 2, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

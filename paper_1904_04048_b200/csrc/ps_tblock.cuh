@@ -76,9 +76,34 @@ constexpr int tb_minb() {
   return 1;
 }
 
+// Narrow windows: stages t >= 1 keep only each lane's own V values per row and fetch the
+// neighbours' R columns by shuffle when a row is used (more shuffles, ~(TS-1)(2R+1)·2R
+// fewer live registers).  Window 0 stays wide (its neighbours come from shared memory).
+#ifndef PS_TB_NARROW
+#define PS_TB_NARROW -1
+#endif
+// Measured: f32 at depth 4 gains (C5 762 -> 834 GLUP/s: 224 -> 168 registers); f64 and
+// depth 2 lose to the extra shuffles.
+template <typename T, class S, int TS>
+__host__ __device__ constexpr bool tb_narrow() {
+  return PS_TB_NARROW >= 0 ? PS_TB_NARROW != 0 : (sizeof(T) == 4 && TS == 4);
+}
+
+// Largest |q2| among the taps of row offset d (how many neighbour columns it reads).
+template <class S>
+__host__ __device__ constexpr int row_need(int d) {
+  int need = 0;
+  for (int s = 0; s < S::N; ++s)
+    if (S::q(s, 0) == d) need = need > (S::q(s, 1) < 0 ? -S::q(s, 1) : S::q(s, 1))
+                                    ? need
+                                    : (S::q(s, 1) < 0 ? -S::q(s, 1) : S::q(s, 1));
+  return need;
+}
+
 template <typename T, int A, class S, int TS, bool PER, int NW, int RB, int NS>
 __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
+  constexpr bool NARROW = tb_narrow<T, S, TS>();
   constexpr int R = S::R;
   using G = TBGeom<T, NW, RB, NS, R, TS>;
   constexpr int V = G::V, HT = G::HT, WO = G::WO, W = G::W, LU = G::LU, LK = G::LK;
@@ -208,6 +233,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
                        bool cols_inner, T* res) {
     constexpr bool INTERIOR = decltype(interior_tag)::value;
     // level k+t+1 at `row` from window t; minus = level k+t-1 at the same row
+    if (NARROW && t > 0) {  // NOLINT
+      // rebuild the neighbour columns of the narrow window by shuffle (only as many as
+      // each row offset's taps read)
+#pragma unroll
+      for (int r = 0; r < 2 * R + 1; ++r) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q < R - row_need<S>(r - R)) continue;   // column never read
+          win[t][r][q] = shfl_up1(win[t][r][R + V - R + q]);
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q >= row_need<S>(r - R)) continue;
+          win[t][r][R + V + q] = shfl_down1(win[t][r][R + q]);
+        }
+      }
+    }
     acc_t acc[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -241,16 +283,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
 
   auto admit = [&](int t, const T* own) {
     // slide window t and admit a new row whose own vector is `own`; neighbours by shuffle
+    // (narrow windows slide only the own columns: their neighbour slots are scratch)
 #pragma unroll
     for (int r = 0; r < 2 * R; ++r)
 #pragma unroll
-      for (int x = 0; x < WC; ++x) win[t][r][x] = win[t][r + 1][x];
+      for (int x = (NARROW ? R : 0); x < (NARROW ? R + V : WC); ++x) win[t][r][x] = win[t][r + 1][x];
 #pragma unroll
     for (int v = 0; v < V; ++v) win[t][2 * R][R + v] = own[v];
+    if constexpr (!NARROW) {  // (narrow windows fetch neighbours when a row is used)
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      win[t][2 * R][q] = shfl_up1(own[V - R + q]);   // left neighbour's last R values
-      win[t][2 * R][R + V + q] = shfl_down1(own[q]);  // right neighbour's first R values
+      for (int q = 0; q < R; ++q) {
+        win[t][2 * R][q] = shfl_up1(own[V - R + q]);   // left neighbour's last R values
+        win[t][2 * R][R + V + q] = shfl_down1(own[q]);  // right neighbour's first R values
+      }
     }
   };
 
