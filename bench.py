@@ -40,7 +40,7 @@ CONFIGS = {
                steps=500, ic=(32, 0.01, 0.05, False), tb=2,
                desc="C3: P13 13-point, 16384^2 f64, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C3f32": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f32", arith="native",
-                  lam=0.4, steps=500, ic=(32, 0.01, 0.05, False), tb=2,
+                  lam=0.4, steps=500, ic=(32, 0.01, 0.05, False), tb=4,
                   desc="C3: P13 13-point, 16384^2 f32, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C4": dict(scheme="P9", n=32767, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.6,
                steps=200, ic=(64, 0.01, 0.05, True), tb=4,
@@ -543,8 +543,8 @@ def main():
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
-                    help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5: "
-                         "4, C3: 2, with an unblocked companion measurement; C1: 1)")
+                    help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
+                         "C3 f32: 4, C3 f64: 2, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.steps is None:

@@ -293,9 +293,9 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 // ---------------------------------------------------------------------------
 // Temporal blocking (ps_tblock.cuh)
 // ---------------------------------------------------------------------------
-// Geometry (measured on B200, profiles/ and DESIGN.md): 4 consumer warps x 3 stages,
-// except f32 at depth 4, whose ~224-register windows allow one block per SM — there 8
-// warps x 2 stages keep more warps resident.  Tuning builds override with -D.
+// Geometry (measured on B200): 4 consumer warps x 3 stages, except f32 at
+// depth 4, whose ~168-register (narrow) windows fit one block per SM — there 8 warps.
+// Tuning builds override with -D.
 #ifndef PS_TB_NW
 #define PS_TB_NW 0
 #endif
@@ -311,7 +311,7 @@ constexpr int tb_nw() {
 }
 template <typename T, int TS>
 constexpr int tb_ns() {
-  return PS_TB_NS > 0 ? PS_TB_NS : ((TS == 4 && sizeof(T) == 4) ? 2 : 3);
+  return PS_TB_NS > 0 ? PS_TB_NS : 3;
 }
 
 template <typename T, int A, class S, int TS, bool PER>
