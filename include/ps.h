@@ -158,9 +158,10 @@ ps_status ps_ipc_close(void* dev_ptr);
 
 /* nsteps two-step updates rotating three levels in place (the loop of run(),
  * simulator.py:271-274).  On entry lvl[*newest] = u^k and lvl[(*newest+2)%3] = u^{k-1};
- * on return *newest names the level holding the last update.  For nsteps >= 6 one
- * rotation cycle (3 launches) is captured into a CUDA graph once and replayed
- * (environment PS_GRAPH=0 disables). */
+ * on return *newest names the level holding the last update.  For nsteps >= 12 six
+ * launches (two rotation cycles) are captured into a CUDA graph once per (grid, levels,
+ * table, phase) and replayed (environment PS_GRAPH=0 disables); odd steps on grids of
+ * <= 256 MB per level walk their tiles bottom-up to reuse the previous step's L2 lines. */
 ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
                    int32_t* newest, void* stream);
 
