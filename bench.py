@@ -540,13 +540,18 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--arith", choices=("ref", "native"), default=None,
+                    help="f32 arithmetic contract override (ref: the reference's numpy "
+                         "sequence with a float64 accumulator; native: one fma per tap)")
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
                     help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
                          "C3 f32: 4, C3 f64: 2, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.arith and cfg["dtype"] == "f32":
+        cfg["arith"] = args.arith
     if args.steps is None:
         args.steps = cfg["steps"]
     args.warmup = max(args.warmup, 0)

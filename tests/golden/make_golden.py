@@ -22,9 +22,9 @@ The GPU parity tests (tests/test_gpu_parity.py) and the oracle pin tests
 
 from __future__ import annotations
 
+import importlib
 import importlib.util
 import json
-import math
 import os
 import sys
 
@@ -47,7 +47,6 @@ def load_reference(src):
 
 def main(src="/root/reference/pkg/src"):
     ref = load_reference(src)
-    sim = sys.modules["ref_poisson_stencils.simulator"]
 
     # ---- tables -----------------------------------------------------------------
     tables = {}
@@ -113,7 +112,6 @@ def main(src="/root/reference/pkg/src"):
     np.savez_compressed(os.path.join(HERE, "fields.npz"), **arrays)
 
     # ---- run() reports for the paper tables ------------------------------------------
-    import importlib
     bench = importlib.import_module("ref_poisson_stencils.benchmarks")
     runs = {"cases": cases, "marches": marches, "tables": {}}
     for t in (1, 2, 3):

@@ -8,7 +8,6 @@ Every test calls through the C-ABI (via the drop-in simulator or the device API)
 from __future__ import annotations
 
 import json
-import math
 import os
 
 import numpy as np
