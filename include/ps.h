@@ -211,6 +211,13 @@ ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, cons
                          double st, double* out2, void* stream);
 void ps_errsum_destroy(ps_errsum* e);
 
+/* run()'s time loop with the fused metric (simulator.py:271-280): nsteps two-step
+ * updates (as ps_march), each followed by ps_errsum_step with st_host[k] (HOST array of
+ * nsteps sine factors) into out_dev[2k..2k+1] (DEVICE).  One call, no per-step host sync. */
+ps_status ps_march_errsum(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
+                          ps_errsum* e, const void* S, const double* st_host, double* out_dev,
+                          int32_t* newest, void* stream);
+
 /* Snapshot writer: one HOST rows x cols block as CSV, "%.17g" per
  * value, "," between values, "\n" after each row — the text of the reference's
  * dump_grid_csv (simulator.py:293-295, np.savetxt) byte for byte, without Python

@@ -54,7 +54,7 @@ EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_
            "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
-           "ps_write_csv",
+           "ps_write_csv", "ps_march_errsum",
            "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
@@ -99,6 +99,8 @@ def load_library(path: str = LIB_PATH):
             "ps_errsum_step": (i32, [vp, G, vp, vp, dbl, vp, vp]),
             "ps_errsum_destroy": (None, [vp]),
             "ps_write_csv": (i32, [ctypes.c_char_p, vp, i64, i64, i64, i32]),
+            "ps_march_errsum": (i32, [G, ctypes.POINTER(vp), i64, T, vp, vp, vp, vp,
+                                      ctypes.POINTER(i32), vp]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
             "ps_version": (ctypes.c_char_p, []),
@@ -319,6 +321,19 @@ class ErrSum:
         check(self._lib.ps_errsum_step(ctypes.c_void_p(self.handle), ctypes.byref(grid),
                                        level.ptr, S.ptr, float(st), ctypes.c_void_p(out_ptr),
                                        stream or current_stream()), "ps_errsum_step")
+
+    def march(self, grid, levels, nsteps: int, t: PsTable, S: Level, st: np.ndarray,
+              out_ptr: int, newest: int, stream=None) -> int:
+        """``nsteps`` updates, each followed by its error sums (ps_march_errsum)."""
+        arr = (ctypes.c_void_p * 3)(*[lv.ptr.value for lv in levels])
+        st = np.ascontiguousarray(st, dtype=np.float64)
+        nw = ctypes.c_int32(newest)
+        check(self._lib.ps_march_errsum(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
+                                        ctypes.c_void_p(self.handle), S.ptr,
+                                        st.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.c_void_p(out_ptr), ctypes.byref(nw),
+                                        stream or current_stream()), "ps_march_errsum")
+        return nw.value
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None

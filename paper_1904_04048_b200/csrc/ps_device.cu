@@ -691,6 +691,21 @@ ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, cons
   return last_cuda_status();
 }
 
+ps_status ps_march_errsum(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
+                          ps_errsum* e, const void* S, const double* st_host, double* out_dev,
+                          int32_t* newest, void* stream) {
+  // run()'s loop (simulator.py:271-280) without a host round trip per step: each
+  // two-step update is followed by its error sums, written to out_dev[2k], out_dev[2k+1].
+  if (!e || !S || !st_host || !out_dev || !lvl || !newest || nsteps < 0) return PS_ERR_ARG;
+  for (int64_t k = 0; k < nsteps; ++k) {
+    ps_status s = ps_march(g, lvl, 1, t, newest, stream);
+    if (s != PS_OK) return s;
+    if ((s = ps_errsum_step(e, g, lvl[*newest], S, st_host[k], out_dev + 2 * k, stream)) != PS_OK)
+      return s;
+  }
+  return PS_OK;
+}
+
 ps_status ps_write_csv(const char* path, const void* host, int64_t rows, int64_t cols,
                        int64_t host_pitch, int32_t dtype) {
   // Host-side writer for dump_grid_csv (simulator.py:293-295: np.savetxt(fmt="%.17g",
