@@ -682,7 +682,7 @@ ps_status ps_errsum_step(ps_errsum* e, const ps_grid* g, const void* level, cons
   if (p.rows_h > g->rows + extra || p.cols_h > g->cols + extra) return PS_ERR_SHAPE;
   cudaStream_t st_ = static_cast<cudaStream_t>(stream);
   const int32_t nvalues = p.nleaves + p.ninternal;
-  k_errsum_leaves<<<unsigned((p.nleaves + 127) / 128), 128, 0, st_>>>(
+  k_errsum_leaves<<<unsigned((int64_t(p.nleaves) * 8 + 255) / 256), 256, 0, st_>>>(
       at_origin<double>(g, level), at_origin<double>(g, S), g->pitch, p.cols_h, st,
       p.leaf_start, p.leaf_len, p.nleaves, p.values, nvalues);
   k_errsum_fold<<<1, 1024, 0, st_>>>(p.node_left, p.node_right, p.node_id, p.level_off,

@@ -40,50 +40,60 @@ __device__ __forceinline__ void errsum_terms(const double* u, const double* S, i
   r2 = __dmul_rn(ref, ref);
 }
 
-__global__ void __launch_bounds__(128)
+// One leaf per 8 lanes: lane j runs numpy's j-th interleaved accumulator (elements
+// j, j+8, j+16, ... of the leaf's multiple-of-8 part), the 8 partial sums combine by
+// shuffle in numpy's fixed order ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), and lane 0 adds the
+// tail sequentially.  Leaves shorter than 8 are summed sequentially from 0.0 by lane 0.
+__global__ void __launch_bounds__(256)
     k_errsum_leaves(const double* __restrict__ u, const double* __restrict__ S, int64_t pitch,
                     int64_t cols_h, double st, const int64_t* __restrict__ leaf_start,
                     const int32_t* __restrict__ leaf_len, int32_t nleaves,
                     double* __restrict__ values, int32_t nvalues) {
-  const int leaf = blockIdx.x * blockDim.x + threadIdx.x;
-  if (leaf >= nleaves) return;
-  const int64_t a = leaf_start[leaf];
-  const int n = leaf_len[leaf];
+  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int leaf = int(gt >> 3), j = int(gt & 7);
+  const bool valid = leaf < nleaves;
+  int64_t a = 0;
+  int n = 0;
+  if (valid) {
+    a = leaf_start[leaf];
+    n = leaf_len[leaf];
+  }
+  const int full = n - (n % 8);
+  double rn = 0.0, rd = 0.0;
+  if (n >= 8) {
+    errsum_terms(u, S, pitch, cols_h, a + j, st, rn, rd);
+    for (int x = 8 + j; x < full; x += 8) {
+      double d2, r2;
+      errsum_terms(u, S, pitch, cols_h, a + x, st, d2, r2);
+      rn = __dadd_rn(rn, d2);
+      rd = __dadd_rn(rd, r2);
+    }
+  }
+  // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) across the leaf's 8 lanes
+#pragma unroll
+  for (int w = 1; w < 8; w <<= 1) {
+    const double on = __shfl_down_sync(0xffffffffu, rn, w, 8);
+    const double od = __shfl_down_sync(0xffffffffu, rd, w, 8);
+    rn = __dadd_rn(rn, on);
+    rd = __dadd_rn(rd, od);
+  }
+  if (!valid || j != 0) return;
   double num, den;
+  int x;
   if (n < 8) {
     num = 0.0;
     den = 0.0;
-    for (int x = 0; x < n; ++x) {
-      double d2, r2;
-      errsum_terms(u, S, pitch, cols_h, a + x, st, d2, r2);
-      num = __dadd_rn(num, d2);
-      den = __dadd_rn(den, r2);
-    }
+    x = 0;
   } else {
-    double rn[8], rd[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) errsum_terms(u, S, pitch, cols_h, a + q, st, rn[q], rd[q]);
-    int x = 8;
-    const int full = n - (n % 8);
-    for (; x < full; x += 8) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        double d2, r2;
-        errsum_terms(u, S, pitch, cols_h, a + x + q, st, d2, r2);
-        rn[q] = __dadd_rn(rn[q], d2);
-        rd[q] = __dadd_rn(rd[q], r2);
-      }
-    }
-    num = __dadd_rn(__dadd_rn(__dadd_rn(rn[0], rn[1]), __dadd_rn(rn[2], rn[3])),
-                    __dadd_rn(__dadd_rn(rn[4], rn[5]), __dadd_rn(rn[6], rn[7])));
-    den = __dadd_rn(__dadd_rn(__dadd_rn(rd[0], rd[1]), __dadd_rn(rd[2], rd[3])),
-                    __dadd_rn(__dadd_rn(rd[4], rd[5]), __dadd_rn(rd[6], rd[7])));
-    for (; x < n; ++x) {
-      double d2, r2;
-      errsum_terms(u, S, pitch, cols_h, a + x, st, d2, r2);
-      num = __dadd_rn(num, d2);
-      den = __dadd_rn(den, r2);
-    }
+    num = rn;
+    den = rd;
+    x = full;
+  }
+  for (; x < n; ++x) {
+    double d2, r2;
+    errsum_terms(u, S, pitch, cols_h, a + x, st, d2, r2);
+    num = __dadd_rn(num, d2);
+    den = __dadd_rn(den, r2);
   }
   values[leaf] = num;
   values[nvalues + leaf] = den;
