@@ -483,7 +483,7 @@ def gpu_arm_dist(args, cfg, cfg_name):
                                       + ", overlapped with the interior update",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": load_traffic(cfg_name),
+                         "frac": achieved / peak, "traffic": load_traffic(cfg_name, T),
                          "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)"},
             "clocks": clk.summary(),
             "gpu_launches": launches,
@@ -545,6 +545,9 @@ def main():
                          "sequence with a float64 accumulator; native: one fma per tap)")
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the torch.distributed row-slab path even at world size 1 "
+                         "(exercises the multi-GPU code on one GPU)")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
                     help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
                          "C3 f32: 4, C3 f64: 2, with an unblocked companion measurement; C1: 1)")
@@ -559,7 +562,7 @@ def main():
     if args.impl == "reference":
         reference_arm(args, cfg, args.config)
         return
-    if world > 1:
+    if world > 1 or args.force_dist:
         gpu_arm_dist(args, cfg, args.config)
     else:
         gpu_arm_single(args, cfg, args.config)
