@@ -225,6 +225,28 @@ ps_status ps_march_errsum(const ps_grid* g, void* lvl[3], int64_t nsteps, const 
 ps_status ps_write_csv(const char* path, const void* host, int64_t rows, int64_t cols,
                        int64_t host_pitch, int32_t dtype);
 
+/* Batched tiny-grid runs: many complete run()s of the paper's tables
+ * (reference benchmarks.py:68-95) in one launch, one CTA per simulation with its three
+ * levels in shared memory (n <= PS_BATCH_MAX_N).  For each simulation the caller packs a
+ * ps_batch_sim into an opaque device descriptor (ps_batch_pack, ps_batch_desc_bytes per
+ * descriptor; copy the array to the device) and concatenates, at the given offsets, the
+ * (n+1)^2 reference-layout arrays u0, v0 (periodic: alias edges consistent) and
+ * S = sin(2πx1)*sin(2πx2), the n_t sine factors st[k-1] = sin(2√2 π c kτ), and room for
+ * 2*n_t outputs.  out receives, per step k, sum((u^k - S*st)^2) and sum((S*st)^2) in
+ * numpy's pairwise order — run()'s per-step error sums, bit for bit. */
+#define PS_BATCH_MAX_N 90
+typedef struct ps_batch_sim {
+  int32_t n, n_t, bc, pad;
+  double tau;
+  ps_table first_u, first_v, two_step;
+  int64_t off_field, off_st, off_out;
+} ps_batch_sim;
+size_t ps_batch_desc_bytes(void);
+ps_status ps_batch_pack(const ps_batch_sim* sim, void* desc_host);
+ps_status ps_batch_run(int32_t nsim, int32_t max_n, const void* desc_dev, const double* u0,
+                       const double* v0, const double* S, const double* st, double* out,
+                       void* stream);
+
 /* Kernel launches issued by this library since load (for launch accounting). */
 int64_t ps_launch_count(void);
 

@@ -48,13 +48,24 @@ class PsTable(ctypes.Structure):
                 ("q2", ctypes.c_int32 * PS_MAX_TAPS), ("c", ctypes.c_double * PS_MAX_TAPS)]
 
 
+class PsBatchSim(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("n_t", ctypes.c_int32), ("bc", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("tau", ctypes.c_double), ("first_u", PsTable),
+                ("first_v", PsTable), ("two_step", PsTable), ("off_field", ctypes.c_int64),
+                ("off_st", ctypes.c_int64), ("off_out", ctypes.c_int64)]
+
+
+PS_BATCH_MAX_N = 90
+
+
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
            "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_two_step_halo",
            "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
-           "ps_write_csv", "ps_march_errsum",
+           "ps_write_csv", "ps_march_errsum", "ps_batch_desc_bytes", "ps_batch_pack",
+           "ps_batch_run",
            "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
@@ -101,6 +112,9 @@ def load_library(path: str = LIB_PATH):
             "ps_write_csv": (i32, [ctypes.c_char_p, vp, i64, i64, i64, i32]),
             "ps_march_errsum": (i32, [G, ctypes.POINTER(vp), i64, T, vp, vp, vp, vp,
                                       ctypes.POINTER(i32), vp]),
+            "ps_batch_desc_bytes": (ctypes.c_size_t, []),
+            "ps_batch_pack": (i32, [ctypes.POINTER(PsBatchSim), vp]),
+            "ps_batch_run": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
             "ps_version": (ctypes.c_char_p, []),
@@ -354,6 +368,28 @@ def write_csv(path, values: np.ndarray):
                                       arr.shape[1], arr.shape[1],
                                       DTYPE["f64" if arr.dtype == np.float64 else "f32"]),
           "ps_write_csv")
+
+
+def batch_run(sims, u0s, v0s, Ss, sts) -> np.ndarray:
+    """Run the packed simulations in one launch; returns the concatenated per-step sums.
+
+    ``sims``: list of PsBatchSim (offsets filled in); the float64 host arrays are the
+    concatenations the offsets refer to."""
+    torch = _torch()
+    lib = load_library()
+    dbytes = lib.ps_batch_desc_bytes()
+    desc = np.zeros(len(sims) * dbytes, dtype=np.uint8)
+    for k, sim in enumerate(sims):
+        check(lib.ps_batch_pack(ctypes.byref(sim), desc[k * dbytes:].ctypes.data_as(ctypes.c_void_p)),
+              "ps_batch_pack")
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to("cuda")  # noqa: E731
+    d_desc, d_u0, d_v0, d_S, d_st = dev(desc), dev(u0s), dev(v0s), dev(Ss), dev(sts)
+    nout = sum(2 * sim.n_t for sim in sims)
+    d_out = torch.empty(nout, dtype=torch.float64, device="cuda")
+    p = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    check(lib.ps_batch_run(len(sims), max(sim.n for sim in sims), p(d_desc), p(d_u0), p(d_v0),
+                           p(d_S), p(d_st), p(d_out), current_stream()), "ps_batch_run")
+    return d_out.cpu().numpy()
 
 
 def launch_count() -> int:

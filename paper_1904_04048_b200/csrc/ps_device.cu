@@ -14,6 +14,7 @@ std::atomic<int64_t> g_launches{0};
 std::atomic<uint64_t> g_launch_seq{0};
 
 #include "ps_errsum.cuh"
+#include "ps_batch.cuh"
 
 static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
                                const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,
@@ -704,6 +705,60 @@ ps_status ps_march_errsum(const ps_grid* g, void* lvl[3], int64_t nsteps, const 
       return s;
   }
   return PS_OK;
+}
+
+static bool batch_table(ps::BatchTable& d, const ps_table& t) {
+  if (t.ntaps < 1 || t.ntaps > PS_MAX_TAPS) return false;
+  d.n = t.ntaps;
+  for (int s = 0; s < t.ntaps; ++s) {
+    if (t.q1[s] < -100 || t.q1[s] > 100 || t.q2[s] < -100 || t.q2[s] > 100) return false;
+    d.q1[s] = int8_t(t.q1[s]);
+    d.q2[s] = int8_t(t.q2[s]);
+    d.c[s] = t.c[s];
+  }
+  return true;
+}
+
+size_t ps_batch_desc_bytes(void) { return sizeof(ps::BatchDev); }
+
+ps_status ps_batch_pack(const ps_batch_sim* sim, void* desc_host) {
+  if (!sim || !desc_host) return PS_ERR_ARG;
+  if (sim->n < 2 || sim->n > PS_BATCH_MAX_N || sim->n_t < 1) return PS_ERR_SHAPE;
+  if (sim->bc != PS_BC_DIRICHLET && sim->bc != PS_BC_PERIODIC) return PS_ERR_ARG;
+  ps::BatchDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.n = sim->n;
+  d.nt = sim->n_t;
+  d.bc = sim->bc;
+  d.tau = sim->tau;
+  if (!batch_table(d.tu, sim->first_u) || !batch_table(d.tv, sim->first_v) ||
+      !batch_table(d.t2, sim->two_step))
+    return PS_ERR_TABLE;
+  d.off_field = sim->off_field;
+  d.off_st = sim->off_st;
+  d.off_out = sim->off_out;
+  std::memcpy(desc_host, &d, sizeof(d));
+  return PS_OK;
+}
+
+ps_status ps_batch_run(int32_t nsim, int32_t max_n, const void* desc_dev, const double* u0,
+                       const double* v0, const double* S, const double* st, double* out,
+                       void* stream) {
+  if (nsim < 1 || !desc_dev || !u0 || !v0 || !S || !st || !out) return PS_ERR_ARG;
+  if (max_n < 2 || max_n > PS_BATCH_MAX_N) return PS_ERR_SHAPE;
+  const size_t nn = size_t(max_n + 1) * size_t(max_n + 1);
+  const size_t smem = 3 * nn * sizeof(double) + 4 * ps::kBatchMaxLeaves * sizeof(double) +
+                      (4 * ps::kBatchMaxLeaves + 2) * sizeof(int);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(ps::k_batch_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+  });
+  if (smem > 227 * 1024) return PS_ERR_SHAPE;
+  ps::k_batch_run<<<unsigned(nsim), ps::kBatchThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const ps::BatchDev*>(desc_dev), u0, v0, S, st, out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return last_cuda_status();
 }
 
 ps_status ps_write_csv(const char* path, const void* host, int64_t rows, int64_t cols,

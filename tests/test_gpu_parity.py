@@ -546,3 +546,20 @@ def test_dropin_is_thread_safe(ps, oracle):
     for (a, b, bc), got in zip(jobs, results):
         want = oracle.two_step(a, b, pairs(spec, "two_step", 0.6), bc, 1)
         assert same_bits(got, want)
+
+
+def test_run_batch_matches_reference_marches(ps, runs):
+    """F4: all golden run() marches in one batched launch, reports bit-identical."""
+    cfgs = [ps.SimConfig(scheme=ps.named_scheme(m["scheme"]), n=m["n"], n_t=m["n_t"],
+                         lam=m["lam"], bc=m["bc"]) for m in runs["marches"]]
+    zero = lambda x1, x2, *_: 0.0 * (x1 + x2)  # noqa: E731
+    cfgs.append(ps.SimConfig(scheme=ps.named_scheme("P5"), n=8, n_t=3, lam=0.5,
+                             exact=lambda x1, x2, t: ps.exact_standing_wave(x1, x2, t)))
+    reports = ps.run_batch(cfgs)
+    for m, rep in zip(runs["marches"], reports):
+        assert rep.error.hex() == m["error"], m["key"]
+        assert [e.hex() for e in rep.per_step_errors] == m["per_step"], m["key"]
+    # the custom-exact config took the run() path and still agrees with the fused one
+    fused = ps.run(ps.SimConfig(scheme=ps.named_scheme("P5"), n=8, n_t=3, lam=0.5))
+    assert reports[-1].error == fused.error
+    del zero
