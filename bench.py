@@ -328,7 +328,12 @@ def gpu_arm_single(args, cfg, cfg_name):
                      "algorithmic_bytes_per_launch": m["bytes_launch"],
                      "kernel_ms_per_launch": m["avg_launch_ms"],
                      "lup_per_launch": m["lup_step"] * T,
-                     "bytes_per_lup": m["words_per_lup"] * sim.itemsize},
+                     "bytes_per_lup": m["words_per_lup"] * sim.itemsize,
+                     **({"note": f"temporal blocking T={T}: the fused kernel moves 4/T words "
+                                 "per update, so it runs below the HBM bound — it is FP64/"
+                                 "FP32 issue-bound (ncu pipe utilisation in profiles/); "
+                                 "lup_roofline compares against the single-update roofline"}
+                        if T > 1 else {})},
         # BASELINE's "fraction of HBM roofline" in update terms: value / (HBM GB/s / 3 words)
         "lup_roofline": {"glups": lup_roofline, "frac": m["value"] / lup_roofline,
                          "note": "single-update roofline (3 words/LUP); temporal blocking "
