@@ -186,6 +186,55 @@ ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
                       int32_t tsteps, int32_t* newest, int32_t* previous, void* stream);
 
+/* Host-to-host solve with the PCIe copies overlapped: the field part
+ * of run() (simulator.py:253-282: u0/v0 in, first step, n_t - 1 two-step updates, the
+ * final level out; dump_grid_csv's input), from HOST arrays to a HOST array.
+ *
+ * Dirichlet grids are cut into row bands marched as a skewed wavefront: band b uploads
+ * its rows of u0/v0, advances every one of its rows through all nsteps levels and
+ * downloads the finished rows while later bands are still uploading or computing, so
+ * the host<->device copies hide behind the stencil work.  Launch j of band b updates
+ * rows [S_b - s(j+1), S_{b+1} - s(j+1)) with a skew s = R*tsteps per launch: every row
+ * it reads above the band was finished for that level by band b-1's launch j-1 and is
+ * not overwritten before band b reads it (ps_solve_plan lists the launches and their
+ * ordering; tests/test_host.py checks the plan for races and replays it on the oracle).
+ * Per-point arithmetic is unchanged, so out equals ps_first_step + ps_march[_tb] bit
+ * for bit.  Periodic grids (rows wrap) run the same sequence unbanded.
+ *
+ * lvl: four device levels of *g (scratch; contents on return unspecified).  u0_host,
+ * v0_host (NULL = zero velocity), out_host: HOST arrays of (rows + a) x (cols + a)
+ * elements with row stride host_pitch, a = 1 for periodic grids (the reference's
+ * alias row/column), 0 for Dirichlet; pinned memory for full copy bandwidth.
+ * nsteps >= 1 = the time level returned (1 = the first step only).  tsteps: temporal
+ * blocking depth (1, 2, 4; reduced to 1 for tables without a fused kernel).
+ * nbands: 0 = auto (about 2048 rows per band).  Returns when the work is enqueued on
+ * `stream`; out_host is valid after the stream synchronises. */
+typedef enum ps_solve_kind {
+  PS_OP_LOAD = 0,   /* host u0 rows -> level dst0, v0 rows -> level dst1 (zeros if NULL) */
+  PS_OP_FIRST = 1,  /* first step: src0 = u0, src1 = v0 -> dst1 = u1                      */
+  PS_OP_STEP = 2,   /* two-step: src0 = u^k, src1 = u^{k-1} -> dst1 = u^{k+1}              */
+  PS_OP_PASS = 3,   /* fused pass: src0 = u^k, src1 = u^{k-1} -> dst0 = u^{k+T-1}, dst1 = u^{k+T} */
+  PS_OP_STORE = 4   /* level src0 rows -> host out                                         */
+} ps_solve_kind;
+typedef struct ps_solve_op {
+  int32_t kind;         /* ps_solve_kind                                                  */
+  int32_t band;
+  int32_t tsteps;       /* updates the op advances (PASS: T; FIRST/STEP: 1; else 0)       */
+  int32_t stream;       /* 0 = upload, 1..nstreams = compute, nstreams + 1 = download     */
+  int32_t src0, src1, dst0, dst1;  /* level indices 0..3, -1 = unused                      */
+  int64_t row_lo, row_hi;          /* logical rows written (LOAD/STEP/...) or read (STORE) */
+  int64_t after0, after1;          /* ops this one waits for besides its stream's order   */
+} ps_solve_op;
+/* The launch plan ps_solve_host executes (host-only; no GPU needed).  Writes up to
+ * max_ops ops and returns how many the plan has (call with ops = NULL to size it), or
+ * -ps_status on bad arguments.  radius = the largest stencil radius of the tables. */
+int64_t ps_solve_plan(int64_t rows, int32_t radius, int64_t nsteps, int32_t tsteps,
+                      int32_t nbands, int32_t nstreams, ps_solve_op* ops, int64_t max_ops);
+ps_status ps_solve_host(const ps_grid* g, void* lvl[4], const void* u0_host,
+                        const void* v0_host, void* out_host, int64_t host_pitch,
+                        const ps_table* tu, const ps_table* tv, const ps_table* t, double tau,
+                        int64_t nsteps, int32_t tsteps, int32_t nbands, void* stream);
+
 /* Sum of K isotropic Gaussians sampled at x1 = i/n, x2 = j/n (the reference's node
  * coordinates np.arange(n+1)/n, simulator.py:254-255) in f64, k order:
  *   u = sum_k amp[k] * exp(-((x1-cx[k])^2 + (x2-cy[k])^2) / (2*(width[k]^2)))

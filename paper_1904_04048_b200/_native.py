@@ -58,6 +58,16 @@ class PsBatchSim(ctypes.Structure):
 PS_BATCH_MAX_N = 90
 
 
+class PsSolveOp(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("band", ctypes.c_int32), ("tsteps", ctypes.c_int32),
+                ("stream", ctypes.c_int32), ("src0", ctypes.c_int32), ("src1", ctypes.c_int32),
+                ("dst0", ctypes.c_int32), ("dst1", ctypes.c_int32), ("row_lo", ctypes.c_int64),
+                ("row_hi", ctypes.c_int64), ("after0", ctypes.c_int64), ("after1", ctypes.c_int64)]
+
+
+SOLVE_KINDS = ("load", "first", "step", "pass", "store")
+
+
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
            "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_two_step_halo",
@@ -65,7 +75,7 @@ EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
            "ps_write_csv", "ps_march_errsum", "ps_batch_desc_bytes", "ps_batch_pack",
-           "ps_batch_run",
+           "ps_batch_run", "ps_solve_plan", "ps_solve_host",
            "ps_launch_count", "ps_strerror", "ps_version")
 
 _lib = None
@@ -115,6 +125,9 @@ def load_library(path: str = LIB_PATH):
             "ps_batch_desc_bytes": (ctypes.c_size_t, []),
             "ps_batch_pack": (i32, [ctypes.POINTER(PsBatchSim), vp]),
             "ps_batch_run": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp]),
+            "ps_solve_plan": (i64, [i64, i32, i64, i32, i32, i32, ctypes.POINTER(PsSolveOp), i64]),
+            "ps_solve_host": (i32, [G, ctypes.POINTER(vp), vp, vp, vp, i64, T, T, T, dbl, i64, i32,
+                                    i32, vp]),
             "ps_launch_count": (i64, []),
             "ps_strerror": (ctypes.c_char_p, [i32]),
             "ps_version": (ctypes.c_char_p, []),
@@ -278,7 +291,7 @@ def ipc_close(ptr: int):
 
 
 def march(grid, levels, nsteps: int, t: PsTable, newest: int, stream=None) -> int:
-    arr = (ctypes.c_void_p * 3)(*[lv.ptr.value for lv in levels])
+    arr = (ctypes.c_void_p * 3)(*[lv.ptr.value for lv in levels[:3]])
     nw = ctypes.c_int32(newest)
     check(load_library().ps_march(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
                                   ctypes.byref(nw), stream or current_stream()), "ps_march")
@@ -308,6 +321,34 @@ def march_tb(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, pr
                                      int(tsteps), ctypes.byref(nw), ctypes.byref(pv),
                                      stream or current_stream()), "ps_march_tb")
     return nw.value, pv.value
+
+
+def solve_plan(rows: int, radius: int, nsteps: int, tsteps: int, nbands: int = 0,
+               nstreams: int = 2) -> list[dict]:
+    """ps_solve_plan as a list of dicts (host-only: works without a GPU)."""
+    L = load_library()
+    n = L.ps_solve_plan(int(rows), int(radius), int(nsteps), int(tsteps), int(nbands),
+                        int(nstreams), None, 0)
+    if n < 0:
+        raise PsStatusError(int(-n), "ps_solve_plan")
+    ops = (PsSolveOp * n)()
+    L.ps_solve_plan(int(rows), int(radius), int(nsteps), int(tsteps), int(nbands), int(nstreams),
+                    ops, n)
+    return [{f: (SOLVE_KINDS[getattr(o, f)] if f == "kind" else getattr(o, f))
+             for f, _ in PsSolveOp._fields_} for o in ops]
+
+
+def solve_host(grid, levels, u0_host, v0_host, out_host, host_pitch: int, tu: PsTable,
+               tv: PsTable, t: PsTable, tau: float, nsteps: int, tsteps: int, nbands: int = 0,
+               stream=None):
+    """ps_solve_host on raw HOST pointers (ints; v0_host may be None = zero velocity)."""
+    arr = (ctypes.c_void_p * 4)(*[lv.ptr.value for lv in levels])
+    check(load_library().ps_solve_host(ctypes.byref(grid), arr, ctypes.c_void_p(u0_host),
+                                       ctypes.c_void_p(v0_host) if v0_host else None,
+                                       ctypes.c_void_p(out_host), int(host_pitch), ctypes.byref(tu),
+                                       ctypes.byref(tv), ctypes.byref(t), float(tau), int(nsteps),
+                                       int(tsteps), int(nbands), stream or current_stream()),
+          "ps_solve_host")
 
 
 def gaussian_sum(grid, level: Level, centres, widths, amps, n: int, stream=None):

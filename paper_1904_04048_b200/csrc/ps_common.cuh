@@ -317,7 +317,7 @@ constexpr int tb_ns() {
 template <typename T, int A, class S, int TS, bool PER>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
-                           cudaStream_t st, bool reverse) {
+                           cudaStream_t st, bool reverse, int rc_hint) {
   constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
@@ -357,6 +357,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   const int resident = std::max(1, dev_info().nsm) * blocks_per_sm;
   p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
   int rc = env_int("PS_TB_ROW_CHUNK", 0);
+  if (rc <= 0) rc = rc_hint;  // banded solve (ps_solve.cuh): its own tile height
   if (rc <= 0) {
     const int64_t want_tiles = int64_t(resident) * 8;
     const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
@@ -385,15 +386,15 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
 template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
-                             cudaStream_t st, bool rev) {
+                             cudaStream_t st, bool rev, int rc) {
   if (shape_matches<ShapeP5>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
   if (shape_matches<ShapeP9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
   if (shape_matches<ShapeC9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
   if (shape_matches<ShapeP13>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
   return PS_ERR_TABLE;
 }
 
@@ -403,24 +404,24 @@ static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1,
 template <typename T, int A, bool PER>
 static ps_status first_step_stream(const ps_grid* g, const void* u0, const void* v0, void* u1,
                                    const ps_table* tu, const ps_table* tv, double tau,
-                                   cudaStream_t st, bool* done) {
+                                   int64_t lo, int64_t hi, cudaStream_t st, bool* done) {
   *done = true;
   const Halo h;
   ps_status s;
   if (shape_matches<ShapeP5>(tv))
-    s = launch_stream<T, A, ShapeP5, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+    s = launch_stream<T, A, ShapeP5, PER, true>(g, v0, v0, u1, tv, lo, hi, st, h, tau);
   else if (shape_matches<ShapeP9>(tv))
-    s = launch_stream<T, A, ShapeP9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+    s = launch_stream<T, A, ShapeP9, PER, true>(g, v0, v0, u1, tv, lo, hi, st, h, tau);
   else if (shape_matches<ShapeC9>(tv))
-    s = launch_stream<T, A, ShapeC9, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+    s = launch_stream<T, A, ShapeC9, PER, true>(g, v0, v0, u1, tv, lo, hi, st, h, tau);
   else if (shape_matches<ShapeP13>(tv))
-    s = launch_stream<T, A, ShapeP13, PER, true>(g, v0, v0, u1, tv, 0, g->rows, st, h, tau);
+    s = launch_stream<T, A, ShapeP13, PER, true>(g, v0, v0, u1, tv, lo, hi, st, h, tau);
   else {
     *done = false;
     return PS_OK;
   }
   if (s != PS_OK) return s;
-  return dispatch_two_step<T, A, PER>(g, u0, u1, u1, tu, 0, g->rows, st, h);
+  return dispatch_two_step<T, A, PER>(g, u0, u1, u1, tu, lo, hi, st, h);
 }
 
 
@@ -433,10 +434,10 @@ static ps_status first_step_stream(const ps_grid* g, const void* u0, const void*
                            const Halo& h);                                                  \
   ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
                      const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev);                                                             \
+                     bool rev, int rc);                                                     \
   ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
-                        const ps_table* tu, const ps_table* tv, double tau, cudaStream_t st, \
-                        bool* done);
+                        const ps_table* tu, const ps_table* tv, double tau, int64_t lo,     \
+                        int64_t hi, cudaStream_t st, bool* done);
 PS_TYPED_DECL(f64)
 PS_TYPED_DECL(f32r)
 PS_TYPED_DECL(f32n)
@@ -450,19 +451,19 @@ PS_TYPED_DECL(f32n)
   }                                                                                         \
   ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
                      const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev) {                                                            \
+                     bool rev, int rc) {                                                    \
     switch (tsteps) {                                                                       \
-      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);         \
-      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev);         \
+      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);     \
+      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);     \
       default: return PS_ERR_ARG;                                                           \
     }                                                                                       \
   }                                                                                         \
   ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
-                        const ps_table* tu, const ps_table* tv, double tau, cudaStream_t st, \
-                        bool* done) {                                                       \
+                        const ps_table* tu, const ps_table* tv, double tau, int64_t lo,     \
+                        int64_t hi, cudaStream_t st, bool* done) {                          \
     return g->bc == PS_BC_PERIODIC                                                          \
-               ? first_step_stream<T, A, true>(g, u0, v0, u1, tu, tv, tau, st, done)        \
-               : first_step_stream<T, A, false>(g, u0, v0, u1, tu, tv, tau, st, done);      \
+               ? first_step_stream<T, A, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done) \
+               : first_step_stream<T, A, false>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done); \
   }
 
 }  // namespace ps

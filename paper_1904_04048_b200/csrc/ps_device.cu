@@ -4,6 +4,7 @@
 //   ps_tblock.cuh   temporal blocking (T fused updates per pass)
 //   ps_generic.cuh  runtime-table kernel, periodic image refresh, Gaussian initial data
 //   ps_errsum.cuh   run()'s per-step error sums in numpy's pairwise order
+//   ps_solve.cuh    host-to-host solve: banded wavefront with the PCIe copies overlapped
 // with ps_arith.cuh (the per-point arithmetic contracts) and ps_ptx.cuh (mbarrier, TMA,
 // PDL primitives).
 #include "ps_common.cuh"
@@ -22,6 +23,11 @@ static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm
   if (g->dtype == PS_F64) return two_step_f64(g, uk, ukm1, ukp1, t, lo, hi, st, h);
   if (g->arith == PS_ARITH_NATIVE) return two_step_f32n(g, uk, ukm1, ukp1, t, lo, hi, st, h);
   return two_step_f32r(g, uk, ukm1, ukp1, t, lo, hi, st, h);
+}
+
+static bool stream_shape(const ps_table* t) {
+  return shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) || shape_matches<ShapeC9>(t) ||
+         shape_matches<ShapeP13>(t);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -46,12 +52,41 @@ static Halo march_opts(const ps_grid* g, int64_t k) {
 
 static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                                   void* ol, const ps_table* t, int tsteps, cudaStream_t st,
-                                  int64_t lo = 0, int64_t hi = -1, bool rev = false) {
+                                  int64_t lo = 0, int64_t hi = -1, bool rev = false,
+                                  int rc = 0) {
   if (hi < 0) hi = g->rows;
-  if (g->dtype == PS_F64) return tb_f64(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev);
+  if (g->dtype == PS_F64) return tb_f64(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
   if (g->arith == PS_ARITH_NATIVE)
-    return tb_f32n(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev);
-  return tb_f32r(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev);
+    return tb_f32n(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
+  return tb_f32r(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
+}
+
+// First step over output rows [lo, hi): two streaming launches for the specialised
+// shapes, the runtime-table kernel otherwise (u1 must not alias u0 or v0 for the former).
+static ps_status first_step_impl(const ps_grid* g, const void* u0, const void* v0, void* u1,
+                                 const ps_table* tu, const ps_table* tv, double tau, int64_t lo,
+                                 int64_t hi, cudaStream_t st) {
+  const bool per = g->bc == PS_BC_PERIODIC;
+  ps_status s = PS_OK;
+  if (u1 != u0 && u1 != v0 && stream_shape(tu) && stream_shape(tv) && g->rows >= 4 &&
+      g->cols >= 4 && env_int("PS_FORCE_GENERIC", 0) == 0) {
+    bool done = false;
+    if (g->dtype == PS_F64)
+      s = first_f64(g, u0, v0, u1, tu, tv, tau, lo, hi, st, &done);
+    else if (g->arith == PS_ARITH_NATIVE)
+      s = first_f32n(g, u0, v0, u1, tu, tv, tau, lo, hi, st, &done);
+    else
+      s = first_f32r(g, u0, v0, u1, tu, tv, tau, lo, hi, st, &done);
+    if (done || s != PS_OK) return s;
+  }
+  if (g->dtype == PS_F64)
+    return per ? launch_generic<double, ARITH_REF, true, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st)
+               : launch_generic<double, ARITH_REF, false, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st);
+  if (g->arith == PS_ARITH_NATIVE)
+    return per ? launch_generic<float, ARITH_NATIVE, true, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st)
+               : launch_generic<float, ARITH_NATIVE, false, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st);
+  return per ? launch_generic<float, ARITH_REF, true, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st)
+             : launch_generic<float, ARITH_REF, false, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st);
 }
 
 static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
@@ -142,11 +177,6 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
   g_graph_next = (g_graph_next + 1) % 32;
   g_ngraphs = std::min(g_ngraphs + 1, 32);
   return exec;
-}
-
-static bool stream_shape(const ps_table* t) {
-  return shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) || shape_matches<ShapeC9>(t) ||
-         shape_matches<ShapeP13>(t);
 }
 
 }  // namespace ps
@@ -289,27 +319,8 @@ ps_status ps_first_step(const ps_grid* g, const void* u0, const void* v0, void* 
   if ((s = check_table(g, tu)) != PS_OK) return s;
   if ((s = check_table(g, tv)) != PS_OK) return s;
   if (!aligned16(u0) || !aligned16(v0) || !aligned16(u1)) return PS_ERR_ALIGN;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const bool per = g->bc == PS_BC_PERIODIC;
-  if (u1 != u0 && u1 != v0 && stream_shape(tu) && stream_shape(tv) && g->rows >= 4 &&
-      g->cols >= 4 && env_int("PS_FORCE_GENERIC", 0) == 0) {
-    bool done = false;
-    if (g->dtype == PS_F64)
-      s = first_f64(g, u0, v0, u1, tu, tv, tau, st, &done);
-    else if (g->arith == PS_ARITH_NATIVE)
-      s = first_f32n(g, u0, v0, u1, tu, tv, tau, st, &done);
-    else
-      s = first_f32r(g, u0, v0, u1, tu, tv, tau, st, &done);
-    if (done || s != PS_OK) return s;
-  }
-  if (g->dtype == PS_F64)
-    return per ? launch_generic<double, ARITH_REF, true, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st)
-               : launch_generic<double, ARITH_REF, false, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st);
-  if (g->arith == PS_ARITH_NATIVE)
-    return per ? launch_generic<float, ARITH_NATIVE, true, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st)
-               : launch_generic<float, ARITH_NATIVE, false, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st);
-  return per ? launch_generic<float, ARITH_REF, true, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st)
-             : launch_generic<float, ARITH_REF, false, true>(g, u0, v0, u1, tu, tv, tau, 0, g->rows, st);
+  return first_step_impl(g, u0, v0, u1, tu, tv, tau, 0, g->rows,
+                         static_cast<cudaStream_t>(stream));
 }
 
 ps_status ps_two_step(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
@@ -808,3 +819,5 @@ const char* ps_strerror(int32_t status) {
 const char* ps_version(void) { return "paper_1904_04048_b200 0.1.0 sm_100a"; }
 
 }  // extern "C"
+
+#include "ps_solve.cuh"

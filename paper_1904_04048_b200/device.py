@@ -136,6 +136,43 @@ class Simulation:
                                                       stream)
         self.step += int(nsteps)
 
+    # ---- host-to-host solve ---------------------------------------------------------
+    def solve_host(self, u0, v0, nsteps: int, out=None, nbands: int = 0, stream=None):
+        """u^nsteps from HOST u0 / v0 (None = zero velocity) into a HOST array, with the
+        uploads, the march and the downloads overlapped band by band (ps_solve_host).
+
+        Arrays are the reference's (n+1)^2 layout as numpy arrays or (preferably pinned)
+        CPU torch tensors of this simulation's dtype.  Blocks until ``out`` is valid and
+        returns it.  The four device levels are scratch: the resident state is reset."""
+        import torch
+
+        if int(nsteps) < 1:
+            raise ValueError("nsteps must be >= 1 (1 = the first step only)")
+        n1 = self.n + 1
+        tdt = torch.float64 if self.dtype == "f64" else torch.float32
+
+        def host(x):
+            t = torch.from_numpy(np.ascontiguousarray(x)) if isinstance(x, np.ndarray) else x
+            if t.dtype != tdt or tuple(t.shape) != (n1, n1) or t.is_cuda:
+                raise ValueError(f"host arrays must be ({n1}, {n1}) {tdt} on the CPU")
+            return t.contiguous()
+
+        u = host(u0)
+        v = None if v0 is None else host(v0)
+        dst = torch.empty((n1, n1), dtype=tdt, pin_memory=True) if out is None else host(out)
+        while len(self.levels) < 4:
+            self.levels.append(nat.Level(self.grid))
+        st = stream or nat.current_stream()
+        nat.solve_host(self.grid, self.levels[:4], u.data_ptr(), None if v is None else v.data_ptr(),
+                       dst.data_ptr(), n1, self.t_first_u, self.t_first_v, self.t_two, self.tau,
+                       int(nsteps), self.tsteps, nbands, st)
+        torch.cuda.synchronize()
+        self.newest = self.previous = None
+        self.step = 0
+        if out is None:
+            return dst.numpy()
+        return out
+
     # ---- read-back ----------------------------------------------------------------
     def field(self, which: str = "newest") -> np.ndarray:
         """Latest (or previous) level as the reference's (n+1)^2 array."""

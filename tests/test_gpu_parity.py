@@ -563,3 +563,63 @@ def test_run_batch_matches_reference_marches(ps, runs):
     fused = ps.run(ps.SimConfig(scheme=ps.named_scheme("P5"), n=8, n_t=3, lam=0.5))
     assert reports[-1].error == fused.error
     del zero
+
+
+# ------------------------------------------------------------ host-to-host banded solve
+@pytest.mark.parametrize("name,n,bc,dtype,arith,T,nbands,nsteps,vzero", [
+    ("P9", 1000, "dirichlet", "f64", "ref", 4, 0, 37, False),
+    ("P9", 1000, "dirichlet", "f64", "ref", 4, 7, 38, True),
+    ("P5", 777, "dirichlet", "f64", "ref", 2, 5, 12, False),
+    ("P13", 903, "dirichlet", "f32", "native", 4, 6, 23, False),
+    ("P13", 903, "dirichlet", "f32", "ref", 2, 3, 9, False),
+    ("P13", 600, "dirichlet", "f64", "ref", 1, 4, 11, True),
+    ("C9", 515, "dirichlet", "f64", "ref", 4, 3, 14, False),
+    ("C13", 515, "dirichlet", "f32", "native", 4, 0, 1, False),
+    ("P9", 64, "dirichlet", "f64", "ref", 4, 9, 30, False),
+    ("P9", 512, "periodic", "f64", "ref", 4, 0, 21, False),
+    ("P13", 300, "periodic", "f32", "native", 2, 0, 6, True),
+])
+def test_solve_host_equals_device_march(name, n, bc, dtype, arith, T, nbands, nsteps, vzero):
+    """ps_solve_host (bands marched as a skewed wavefront, uploads/downloads overlapped on
+    side streams) returns the same bits as upload + first step + march + download."""
+    from paper_1904_04048_b200.device import Simulation
+
+    lam = 0.4 if name in ("P13", "C13") else 0.6
+    npdt = np.float64 if dtype == "f64" else np.float32
+    rng = np.random.default_rng(n + nsteps)
+    u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    v0 = None if vzero else rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    if bc == "periodic":
+        for f in (u0, v0):
+            if f is not None:
+                f[:-1, -1] = f[:-1, 0]
+                f[-1, :] = f[0, :]
+    sim = Simulation(name, n, lam, bc=bc, dtype=dtype, arith=arith, tsteps=T)
+    sim.load_initial(u0, v0)
+    sim.first_step()
+    if nsteps > 1:
+        sim.march(nsteps - 1)
+    want = sim.field()
+    got = sim.solve_host(u0, v0, nsteps, nbands=nbands)
+    assert same_bits(got, want)
+    # again into a caller buffer, after the levels hold stale data
+    out = np.empty_like(u0)
+    sim.solve_host(u0, v0, nsteps, out=out, nbands=nbands)
+    assert same_bits(out, want)
+
+
+def test_solve_host_full_c4_checksum():
+    """C4 at full size through ps_solve_host (auto bands, T=4, 16 steps) against the
+    resident march: identical bytes of the 8.6 GB result."""
+    import torch
+
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation("P9", 32767, 0.6, bc="dirichlet", ring=1, dtype="f64", tsteps=4)
+    sim.gaussian_initial(64, 0.01, 0.05, seed=0, v_zero=True)
+    u0 = torch.from_numpy(sim.levels[1].download(32768, 32768)).pin_memory()
+    sim.first_step()
+    sim.march(15)
+    want = torch.from_numpy(sim.field())
+    got = torch.from_numpy(sim.solve_host(u0, None, 16))
+    assert torch.equal(got.view(torch.int64), want.view(torch.int64))
