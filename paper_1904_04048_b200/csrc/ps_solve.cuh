@@ -14,9 +14,9 @@
 // launch's read reach.  Then
 //   * rows launch j of band b reads above its range (>= S_b - o_j - s) hold launch j-1's
 //     output there: band b-1's launch j-1 wrote up to S_b - o_{j-1}, and band b-1's
-//     launches >= j+1 only write below S_b - o_{j+1} = S_b - o_j - s;
+//     launches >= j+1 only write below S_b - o_{j+1} = S_b - o_j - s (bands are at
+//     least 2s rows tall, so those rows lie in band b-1's range);
 //   * rows it reads below its range come from band b's own launch j-1;
-//     (bands are at least 2s rows tall, so those rows lie in band b-1);
 //   * so launch (b, j) needs (b, j-1) and (b-1, j-1) — nothing else — and band b-1 may
 //     run ahead of band b; each launch's outputs never alias the inputs it reads at
 //     neighbour rows (fused passes and tail steps write free levels; the first step's
