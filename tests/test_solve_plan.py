@@ -211,3 +211,37 @@ def test_solve_plan_replay_equals_unbanded_march(O, name, n, nsteps, T, nb):
         got = _replay(O, ops, u0, v0, pu, pv, p2, tau, ring, list(order))
         assert not np.isnan(got).any()
         assert got.tobytes() == want.tobytes()
+
+
+def test_solve_host_rejects_bad_arguments_before_touching_the_gpu():
+    """ps_solve_host validates everything before its first CUDA call (runs without a GPU)."""
+    import ctypes
+
+    L = nat.load_library()
+    g = nat.make_grid(65, 65, 2, 1, "dirichlet", "f64")
+    spec = named_scheme("P9")
+    t = nat.make_table(evaluate_table(spec.two_step, 0.6))
+    tu = nat.make_table(evaluate_table(spec.first_u, 0.6))
+    tv = nat.make_table(evaluate_table(spec.first_v, 0.6))
+    host = np.zeros((65, 65))
+    hp = host.ctypes.data
+    good = (ctypes.c_void_p * 4)(4096, 8192, 12288, 16384)   # never dereferenced on error
+
+    def call(lv=good, u0=hp, out=hp, pitch=65, nsteps=5, tsteps=4, nbands=0, grid=g,
+             tt=t):
+        return L.ps_solve_host(ctypes.byref(grid), lv, ctypes.c_void_p(u0), None,
+                               ctypes.c_void_p(out), pitch, ctypes.byref(tu), ctypes.byref(tv),
+                               ctypes.byref(tt), 0.01, nsteps, tsteps, nbands, None)
+
+    assert call(nsteps=0) == 1
+    assert call(tsteps=3) == 1
+    assert call(nbands=-1) == 1
+    assert call(u0=0) == 1
+    assert call(out=0) == 1
+    assert call(pitch=10) == 1
+    assert call(lv=(ctypes.c_void_p * 4)(4096, 4096, 12288, 16384)) == 1   # aliased levels
+    assert call(lv=(ctypes.c_void_p * 4)(4100, 8192, 12288, 16384)) == 6   # misaligned
+    wide = nat.make_table(evaluate_table(named_scheme("P13").two_step, 0.4))
+    assert call(tt=wide) == 4                                              # radius > ring
+    slab = nat.make_slab_grid(130, 65, 65, 65, 2, 1, "dirichlet", "f64")
+    assert call(grid=slab) == 2
