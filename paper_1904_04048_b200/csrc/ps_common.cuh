@@ -293,9 +293,8 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 // ---------------------------------------------------------------------------
 // Temporal blocking (ps_tblock.cuh)
 // ---------------------------------------------------------------------------
-// Geometry (measured on B200): 4 consumer warps x 3 stages, except f32 at
-// depth 4, whose ~168-register (narrow) windows fit one block per SM — there 8 warps.
-// Tuning builds override with -D.
+// Geometry (measured on B200, tools/tb_variants.sh): 11 consumer warps + 1
+// producer warp, one block per SM, 3 pipeline stages.  Tuning builds override with -D.
 #ifndef PS_TB_NW
 #define PS_TB_NW 0
 #endif
@@ -307,7 +306,7 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #endif
 template <typename T, int TS>
 constexpr int tb_nw() {
-  return PS_TB_NW > 0 ? PS_TB_NW : ((TS == 4 && sizeof(T) == 4) ? 8 : 4);
+  return PS_TB_NW > 0 ? PS_TB_NW : 11;
 }
 template <typename T, int TS>
 constexpr int tb_ns() {

@@ -65,15 +65,14 @@ __device__ __forceinline__ T shfl_down1(T x) {
 #ifndef PS_TB_MINB
 #define PS_TB_MINB 0  // tuning override: minimum resident blocks per SM (caps registers)
 #endif
-// Measured (tools/): asking for 3 resident blocks (<= 136 registers) pays
-// for f32 at depth 2 (+2-4 %) and radius-1 f64 Dirichlet at depth 4 (+4 %); elsewhere
-// the extra spills cost more than the occupancy gains.
+// Measured (tools/tb_variants.sh): one block of 11 consumer warps + the
+// producer per SM beats 3 blocks of 4 + 1 everywhere (C4 468 -> 514, C5 902 -> 1008,
+// C3 f64 T=2 321 -> 366 GLUP/s): 12 warps leave 168 registers per thread (3 warps share a
+// sub-partition's 16K registers), so the windows fit without spills, and one block keeps
+// the whole strip's halo columns in one shared-memory ring.
 template <typename T, class S, int TS, bool PER>
 constexpr int tb_minb() {
-  if (PS_TB_MINB > 0) return PS_TB_MINB;
-  if (sizeof(T) == 4 && TS == 2) return 3;
-  if (sizeof(T) == 8 && S::R == 1 && TS == 4 && !PER) return 3;
-  return 1;
+  return PS_TB_MINB > 0 ? PS_TB_MINB : 1;
 }
 
 // Narrow windows: stages t >= 1 keep only each lane's own V values per row and fetch the
