@@ -569,7 +569,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="C4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--bands", type=int, default=0,
-                    help="row bands of the e2e solve (0 = auto, ~2048 rows each)")
+                    help="row bands of the e2e solve (0 = auto, ~1024 rows each)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--arith", choices=("ref", "native"), default=None,

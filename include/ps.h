@@ -207,7 +207,7 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
  * alias row/column), 0 for Dirichlet; pinned memory for full copy bandwidth.
  * nsteps >= 1 = the time level returned (1 = the first step only).  tsteps: temporal
  * blocking depth (1, 2, 4; reduced to 1 for tables without a fused kernel).
- * nbands: 0 = auto (about 2048 rows per band).  Returns when the work is enqueued on
+ * nbands: 0 = auto (about 1024 rows per band).  Returns when the work is enqueued on
  * `stream`; out_host is valid after the stream synchronises. */
 typedef enum ps_solve_kind {
   PS_OP_LOAD = 0,   /* host u0 rows -> level dst0, v0 rows -> level dst1 (zeros if NULL) */

@@ -37,7 +37,9 @@ struct SolvePlanIn {
 };
 
 static int64_t solve_auto_bands(int64_t rows, int s) {
-  int64_t B = (rows + 1024) / 2048;  // about 2048 rows per band
+  // about 1024 rows per band (C4 sweep, profiles/r01_solve_tune_c4.jsonl: 16 bands 461,
+  // 32 bands 468 GLUP/s host-to-host; the fill and drain shrink with the band)
+  int64_t B = (rows + 512) / 1024;
   B = std::min<int64_t>(B, 64);
   B = std::min<int64_t>(B, rows / std::max<int64_t>(1, 8 * s));  // bands >= 8 skews tall
   return std::max<int64_t>(B, 1);

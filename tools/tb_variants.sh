@@ -16,8 +16,9 @@ NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcomp
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
-  [nw11]="-DPS_TB_NW=11 -DPS_TB_MINB=1"
-  [nw7]="-DPS_TB_NW=7 -DPS_TB_MINB=1"
+  [ns2]="-DPS_TB_NS=2"
+  [ns4]="-DPS_TB_NS=4"
+  [rb2]="-DPS_TB_RB=2"
 )
 if [ "${MODE:-build}" = build ]; then
   make -s -j4 paper_1904_04048_b200/libps.so
