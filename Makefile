@@ -10,7 +10,7 @@ UNITS = ps_device ps_kern_f64 ps_kern_f32r ps_kern_f32n
 OBJS = $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDR = include/ps.h $(wildcard $(CSRC)/*.cuh)
 
-all: paper_1904_04048_b200/libps.so oracle
+all: paper_1904_04048_b200/libps.so build/fp64_probe oracle
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
@@ -18,6 +18,11 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDR)
 
 paper_1904_04048_b200/libps.so: $(OBJS)
 	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -o $@ $(OBJS)
+
+# compute-roofline probe (FP64 add / FP32 fma rates) run by bench.py
+build/fp64_probe: tools/fp64_probe.cu
+	@mkdir -p build
+	$(NVCC) -O3 -gencode arch=compute_100a,code=sm_100a -o $@ $<
 
 oracle:
 	$(MAKE) -C oracle

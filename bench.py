@@ -62,6 +62,38 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def compute_roofline(cfg, value_glups):
+    """Arithmetic roofline of the fused kernel (temporal blocking makes it instruction-bound,
+    not HBM-bound): FP-pipe instructions per update under the config's contract times the
+    update rate, against the DADD (f64) / FFMA (f32) throughput tools/fp64_probe.cu measures
+    on this GPU in this run.  None if the probe binary is absent."""
+    import subprocess
+
+    from paper_1904_04048_b200.scheme import named_scheme
+
+    probe = os.path.join(ROOT, "build", "fp64_probe")
+    if not os.path.exists(probe) or cfg["arith"] == "ref" and cfg["dtype"] == "f32":
+        return None
+    try:
+        out = subprocess.run([probe], capture_output=True, text=True, timeout=60, check=True)
+        rates = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+    ntaps = len(named_scheme(cfg["scheme"]).two_step)
+    if cfg["dtype"] == "f64":   # reference contract: one DMUL + one DADD per tap, one DSUB
+        ipl, peak, pipe = 2 * ntaps + 1, rates["dadd_rate_32warps_per_sm_Gops"], "fp64"
+    else:                       # native f32: one FFMA per tap, one FADD
+        ipl, peak, pipe = ntaps + 1, rates["ffma_rate_Gops"], "fp32"
+    achieved = value_glups * ipl
+    return {"bound": f"{pipe} pipe", "achieved": achieved, "peak": peak,
+            "unit": "G thread-instructions/s", "frac": achieved / peak,
+            "instr_per_lup": ipl,
+            "peak_source": "measured in this run: tools/fp64_probe.cu "
+                           f"({'DADD' if pipe == 'fp64' else 'FFMA'} throughput, all SMs)",
+            "note": "algorithmic instructions only (no recomputed halo columns/rows); the "
+                    "reference's order fixes a dependent add chain per update"}
+
+
 def load_traffic(cfg_name, T=1):
     path = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}" + (f"_T{T}" if T > 1 else "") + ".json")
     try:
@@ -341,6 +373,8 @@ def gpu_arm_single(args, cfg, cfg_name):
         "clocks": m["clocks"],
         "gpu_launches": m["launches"],
     }
+    if T > 1:
+        line["compute_roofline"] = compute_roofline(cfg, m["value"])
     if companion:
         line["unblocked_companion"] = companion
     if not args.no_e2e:

@@ -1,7 +1,8 @@
 // fp64_probe.cu — measures the B200's FP64 add latency (one warp, one dependent chain)
-// and throughput (all SMs, many independent chains), and the 32-bit shuffle latency,
-// to size the temporal-blocking kernel's instruction-level parallelism.
-//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o build/fp64_probe tools/fp64_probe.cu
+// and the FP64 add / FP32 fma instruction throughput (all SMs, many independent chains),
+// plus the 32-bit shuffle latency: the compute roofline of the fused (temporally blocked)
+// kernels, which are arithmetic-bound.  bench.py runs it and reports the rates.
+//   make build/fp64_probe   (nvcc -O3 -gencode arch=compute_100a,code=sm_100a)
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -27,6 +28,21 @@ __global__ void lat_shfl(float* out, float a, int iters, long long* cyc) {
   long long t1 = clock64();
   if (threadIdx.x == 0) *cyc = t1 - t0;
   out[threadIdx.x] = x;
+}
+
+template <int CH>
+__global__ void thr_ffma(float* out, float a, int iters) {
+  float x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = a * (c + 1 + threadIdx.x);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = __fmaf_rn(x[c], a, 0.5f);
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
 template <int CH>
@@ -74,6 +90,18 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     const double ops = double(blocks) * threads * it * 8;
     printf("\"dadd_rate_%dwarps_per_sm_Gops\": %.1f, ", warps, ops / (ms * 1e-3) / 1e9);
+  }
+  {
+    const int blocks = nsm * 8, threads = 256, it = 20000;
+    thr_ffma<8><<<blocks, threads>>>(reinterpret_cast<float*>(out), 1.0001f, 10);
+    cudaEventRecord(e0);
+    thr_ffma<8><<<blocks, threads>>>(reinterpret_cast<float*>(out), 1.0001f, it);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = double(blocks) * threads * it * 8;
+    printf("\"ffma_rate_Gops\": %.1f, ", ops / (ms * 1e-3) / 1e9);
   }
   printf("\"nsm\": %d, \"clock_khz\": %d}\n", nsm, clk);
   return 0;
