@@ -484,8 +484,6 @@ def gpu_arm_dist(args, cfg, cfg_name):
         raise SystemExit("multi-GPU bench supports the Dirichlet Gaussian configs (C3-C5)")
     K = args.steps
     T = args.tsteps if args.tsteps > 0 else cfg.get("tb", 1)
-    if args.transport != "nccl":
-        T = 1
     while T > 1 and K % T:      # the timed region must hold whole blocked passes
         T //= 2
     slab = DistributedSlabs(cfg["scheme"], cfg["n"], cfg["lam"], ring=cfg["ring"],
@@ -543,7 +541,8 @@ def gpu_arm_dist(args, cfg, cfg_name):
                        "lambda": cfg["lam"], "arith": cfg["arith"], "temporal_blocking": T,
                        "parallelism": f"row slabs x{world}, {slab.R * T}-row halo "
                                       + ("over NCCL send/recv" if args.transport == "nccl" else
-                                         "stored into peer ghost rows by the kernel (CUDA IPC)")
+                                         "stored into peer ghost rows by the fused kernel "
+                                         "(CUDA IPC over NVLink)")
                                       + ", overlapped with the interior update",
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -562,24 +561,37 @@ def e2e_dist(args, cfg, slab, dist, ics):
     step, K-1 steps, own rows of u^K -> pinned host; time = max over ranks."""
     import torch
 
+    import ctypes
+
+    from paper_1904_04048_b200 import _native as nat
+
     u_host, v_host = ics
     out = torch.empty_like(u_host).pin_memory()
     K = args.steps
+    lib, g, st = nat.load_library(), slab.grid, nat.current_stream()
+    rows, cols = u_host.shape
+
+    def copy_in(level, host):   # cudaMemcpy2DAsync into the padded layout (pinned source)
+        nat.check(lib.ps_copy_in(ctypes.byref(g), level.ptr, ctypes.c_void_p(host.data_ptr()),
+                                 rows, cols, cols, nat.H2D, st), "ps_copy_in")
+
     torch.cuda.synchronize()
     dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record()
-    slab.levels[1].view().copy_(u_host, non_blocking=True)
+    copy_in(slab.levels[1], u_host)
     if v_host is None:
         slab.levels[0].buf.zero_()
     else:
-        slab.levels[0].view().copy_(v_host, non_blocking=True)
+        copy_in(slab.levels[0], v_host)
     slab.exchange(1)
     slab.exchange(0)
     slab.first_step()
     more = (K - 1) // slab.T * slab.T          # whole blocked passes after the first step
     slab.march(more)
-    out.copy_(slab.levels[slab.newest].view(), non_blocking=True)
+    nat.check(lib.ps_copy_out(ctypes.byref(g), slab.levels[slab.newest].ptr,
+                              ctypes.c_void_p(out.data_ptr()), rows, cols, cols, nat.D2H, st),
+              "ps_copy_out")
     t1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")

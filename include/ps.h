@@ -180,6 +180,20 @@ ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1
                               void* out_prev, void* out_last, const ps_table* t, int32_t tsteps,
                               int64_t row_lo, int64_t row_hi, void* stream);
 
+/* ps_two_step_tb_rows with in-kernel halo delivery (the fused pass +
+ * exchange over NVLink peer memory): the CTAs that write out_last rows [0, R*tsteps) and
+ * [rows - R*tsteps, rows), and out_prev rows [0, R*(tsteps-1)) and [rows - R*(tsteps-1),
+ * rows), also store them into the neighbour slabs' ghost rows — up_prev / up_last (the
+ * slab above's out_prev / out_last levels, `up_rows` logical rows) at rows up_rows + r,
+ * dn_prev / dn_last (the slab below's) at rows r - rows.  Peer pointers are allocation
+ * bases (ps_ipc_open) on devices reachable by peer access; NULL = no neighbour (both of a
+ * side or neither).  Dirichlet slabs, ghost >= R*tsteps.  The caller orders the next pass
+ * after the neighbours' boundary launches (event / NCCL token). */
+ps_status ps_two_step_tb_halo(const ps_grid* g, const void* uk, const void* ukm1,
+                              void* out_prev, void* out_last, const ps_table* t, int32_t tsteps,
+                              int64_t row_lo, int64_t row_hi, void* up_prev, void* up_last,
+                              int64_t up_rows, void* dn_prev, void* dn_last, void* stream);
+
 /* nsteps updates over four rotating levels with temporal blocking depth tsteps (1, 2, 4);
  * lvl[*newest] = u^k and lvl[*previous] = u^{k-1} on entry and on return.  nsteps not
  * divisible by tsteps finishes with single steps. */

@@ -71,6 +71,7 @@ SOLVE_KINDS = ("load", "first", "step", "pass", "store")
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
            "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_two_step_halo",
+           "ps_two_step_tb_halo",
            "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
            "ps_gaussian_sum", "ps_errsum_create", "ps_errsum_step", "ps_errsum_destroy",
@@ -110,6 +111,8 @@ def load_library(path: str = LIB_PATH):
             "ps_two_step_tb": (i32, [G, vp, vp, vp, vp, T, i32, vp]),
             "ps_two_step_halo": (i32, [G, vp, vp, vp, T, i64, i64, vp, i64, vp, vp]),
             "ps_two_step_tb_rows": (i32, [G, vp, vp, vp, vp, T, i32, i64, i64, vp]),
+            "ps_two_step_tb_halo": (i32, [G, vp, vp, vp, vp, T, i32, i64, i64, vp, vp, i64, vp,
+                                          vp, vp]),
             "ps_ipc_get_handle": (i32, [vp, vp, ctypes.POINTER(i64)]),
             "ps_ipc_open": (i32, [vp, ctypes.POINTER(vp)]),
             "ps_ipc_close": (i32, [vp]),
@@ -311,6 +314,22 @@ def two_step_tb_rows(grid, uk: Level, ukm1: Level, out_prev: Level, out_last: Le
                                              out_last.ptr, ctypes.byref(t), int(tsteps), int(lo),
                                              int(hi), stream or current_stream()),
           "ps_two_step_tb_rows")
+
+
+def two_step_tb_halo(grid, uk: Level, ukm1: Level, out_prev: Level, out_last: Level,
+                     t: PsTable, tsteps: int, lo: int, hi: int, up: tuple | None, up_rows: int,
+                     dn: tuple | None, stream=None):
+    """Fused pass over rows [lo, hi) that also stores its boundary rows of both output
+    levels into the neighbours' ghost rows (``up`` / ``dn``: (out_prev, out_last)
+    allocation base pointers of the neighbour slab, or None)."""
+    vp = ctypes.c_void_p
+    u = up or (0, 0)
+    d = dn or (0, 0)
+    check(load_library().ps_two_step_tb_halo(ctypes.byref(grid), uk.ptr, ukm1.ptr, out_prev.ptr,
+                                             out_last.ptr, ctypes.byref(t), int(tsteps), int(lo),
+                                             int(hi), vp(u[0]), vp(u[1]), int(up_rows), vp(d[0]),
+                                             vp(d[1]), stream or current_stream()),
+          "ps_two_step_tb_halo")
 
 
 def march_tb(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, previous: int,

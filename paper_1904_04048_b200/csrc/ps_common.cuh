@@ -150,6 +150,16 @@ static bool single_slab(const ps_grid* g) { return g->row0 == 0 && g->grows == g
 
 // Peer halo targets of a row-slab update (logical-origin pointers of the neighbours'
 // u^{k+1} levels; null = no neighbour / exchange done elsewhere).
+// Peer halo targets of a temporally blocked row-slab pass (allocation bases of the
+// neighbours' out_prev / out_last levels, as from ps_ipc_open; null = none).
+struct TBHalo {
+  void* up_prev = nullptr;
+  void* up_last = nullptr;
+  void* dn_prev = nullptr;
+  void* dn_last = nullptr;
+  int32_t up_rows = 0;
+};
+
 struct Halo {
   void* up = nullptr;
   void* dn = nullptr;
@@ -316,7 +326,7 @@ constexpr int tb_ns() {
 template <typename T, int A, class S, int TS, bool PER>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
-                           cudaStream_t st, bool reverse, int rc_hint) {
+                           cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
   constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
@@ -349,6 +359,11 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.gmax = int32_t(g->rows + g->ghost);
   p.cmax = int32_t(g->pitch - (g->origin - g->ghost * g->pitch));
   p.reverse = reverse ? 1 : 0;
+  p.hu_prev = h.up_prev ? at_origin<T>(g, h.up_prev) : nullptr;
+  p.hu_last = h.up_last ? at_origin<T>(g, h.up_last) : nullptr;
+  p.hd_prev = h.dn_prev ? at_origin<T>(g, h.dn_prev) : nullptr;
+  p.hd_last = h.dn_last ? at_origin<T>(g, h.dn_last) : nullptr;
+  p.up_rows = h.up_rows;
   for (int s = 0; s < S::N; ++s) {
     p.c[s] = t->c[s];
     p.cf[s] = static_cast<float>(t->c[s]);
@@ -385,15 +400,15 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
 template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
-                             cudaStream_t st, bool rev, int rc) {
+                             cudaStream_t st, bool rev, int rc, const TBHalo& h) {
   if (shape_matches<ShapeP5>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeC9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP13>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);
+    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   return PS_ERR_TABLE;
 }
 
@@ -433,7 +448,7 @@ static ps_status first_step_stream(const ps_grid* g, const void* u0, const void*
                            const Halo& h);                                                  \
   ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
                      const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev, int rc);                                                     \
+                     bool rev, int rc, const TBHalo& h);                                    \
   ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
                         const ps_table* tu, const ps_table* tv, double tau, int64_t lo,     \
                         int64_t hi, cudaStream_t st, bool* done);
@@ -450,10 +465,10 @@ PS_TYPED_DECL(f32n)
   }                                                                                         \
   ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
                      const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev, int rc) {                                                    \
+                     bool rev, int rc, const TBHalo& h) {                                   \
     switch (tsteps) {                                                                       \
-      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);     \
-      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc);     \
+      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
+      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
       default: return PS_ERR_ARG;                                                           \
     }                                                                                       \
   }                                                                                         \

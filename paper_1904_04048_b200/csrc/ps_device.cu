@@ -53,12 +53,12 @@ static Halo march_opts(const ps_grid* g, int64_t k) {
 static ps_status two_step_tb_impl(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                                   void* ol, const ps_table* t, int tsteps, cudaStream_t st,
                                   int64_t lo = 0, int64_t hi = -1, bool rev = false,
-                                  int rc = 0) {
+                                  int rc = 0, const TBHalo& h = TBHalo{}) {
   if (hi < 0) hi = g->rows;
-  if (g->dtype == PS_F64) return tb_f64(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
+  if (g->dtype == PS_F64) return tb_f64(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc, h);
   if (g->arith == PS_ARITH_NATIVE)
-    return tb_f32n(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
-  return tb_f32r(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc);
+    return tb_f32n(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc, h);
+  return tb_f32r(g, uk, ukm1, op, ol, t, tsteps, lo, hi, st, rev, rc, h);
 }
 
 // First step over output rows [lo, hi): two streaming launches for the specialised
@@ -474,6 +474,40 @@ ps_status ps_two_step_tb_rows(const ps_grid* g, const void* uk, const void* ukm1
     return PS_ERR_ALIGN;
   return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
                           static_cast<cudaStream_t>(stream), row_lo, row_hi);
+}
+
+ps_status ps_two_step_tb_halo(const ps_grid* g, const void* uk, const void* ukm1,
+                              void* out_prev, void* out_last, const ps_table* t, int32_t tsteps,
+                              int64_t row_lo, int64_t row_hi, void* up_prev, void* up_last,
+                              int64_t up_rows, void* dn_prev, void* dn_last, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (g->bc != PS_BC_DIRICHLET) return PS_ERR_ARG;
+  if (!uk || !ukm1 || !out_prev || !out_last) return PS_ERR_ARG;
+  if (out_prev == uk || out_prev == ukm1 || out_last == uk || out_last == ukm1 ||
+      out_prev == out_last)
+    return PS_ERR_ARG;
+  if (row_lo < 0 || row_hi > g->rows || row_lo > row_hi) return PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  if (!tb_supported(g, t, tsteps) || tsteps < 2) return PS_ERR_ARG;
+  const int64_t depth = int64_t(table_radius(t)) * tsteps;
+  if (depth > g->ghost || depth > g->rows) return PS_ERR_SHAPE;
+  if ((up_prev != nullptr) != (up_last != nullptr) || (dn_prev != nullptr) != (dn_last != nullptr))
+    return PS_ERR_ARG;
+  if (up_prev && up_rows < depth) return PS_ERR_ARG;
+  for (const void* q : {uk, ukm1, static_cast<const void*>(out_prev),
+                        static_cast<const void*>(out_last), static_cast<const void*>(up_prev),
+                        static_cast<const void*>(up_last), static_cast<const void*>(dn_prev),
+                        static_cast<const void*>(dn_last)})
+    if (q && !aligned16(q)) return PS_ERR_ALIGN;
+  TBHalo h;
+  h.up_prev = up_prev;
+  h.up_last = up_last;
+  h.dn_prev = dn_prev;
+  h.dn_last = dn_last;
+  h.up_rows = int32_t(up_rows);
+  return two_step_tb_impl(g, uk, ukm1, out_prev, out_last, t, tsteps,
+                          static_cast<cudaStream_t>(stream), row_lo, row_hi, false, 0, h);
 }
 
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,

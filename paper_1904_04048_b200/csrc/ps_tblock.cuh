@@ -34,6 +34,15 @@ struct TBParams {
   int32_t cmax;            // loadable columns: element index < cmax (from logical col 0)
   int32_t nstrips, rc, ntiles;
   int32_t reverse;         // walk tiles bottom-up (alternate launches: L2 reuse)
+  // row slabs with in-kernel halo delivery (logical-origin pointers of the neighbours'
+  // out_prev / out_last levels, null = none): out_last rows [0, R*TS) also land in the
+  // slab above at rows up_rows + r, rows [rows - R*TS, rows) in the slab below at r - rows;
+  // out_prev likewise with depth R*(TS-1)
+  void* hu_prev;
+  void* hu_last;
+  void* hd_prev;
+  void* hd_last;
+  int32_t up_rows;
   double c[PS_MAX_TAPS];
   float cf[PS_MAX_TAPS];
 };
@@ -316,14 +325,28 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     for (int v = 0; v < V; ++v) win[0][2 * R][R + v] = o[v];
   };
 
-  auto store_vec = [&](T* base, int row, int gc0, const T* res) {
-    T* dst = base + int64_t(row) * pitch + gc0;
+  auto put = [&](T* dst, int gc0, const T* res) {
     if (gc0 + V <= p.cols) {
       *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v)
         if (gc0 + v < p.cols) dst[v] = res[v];
+    }
+  };
+  // last = true: out_last (halo depth R*TS), else out_prev (depth R*(TS-1))
+  auto store_vec = [&](T* base, int row, int gc0, const T* res, bool last) {
+    put(base + int64_t(row) * pitch + gc0, gc0, res);
+    if constexpr (!PER) {
+      // fused halo delivery: boundary rows also go straight into the neighbours' ghost
+      // rows (peer memory over NVLink, ps_two_step_tb_halo)
+      void* hu = last ? p.hu_last : p.hu_prev;
+      void* hd = last ? p.hd_last : p.hd_prev;
+      const int depth = last ? R * TS : R * (TS - 1);
+      if (hu && row < depth)
+        put(static_cast<T*>(hu) + int64_t(p.up_rows + row) * pitch + gc0, gc0, res);
+      if (hd && row >= p.rows - depth)
+        put(static_cast<T*>(hd) + int64_t(row - p.rows) * pitch + gc0, gc0, res);
     }
     if constexpr (PER) {
       // refresh wrap-around images to depth D = R*TS (what the next pass loads)
@@ -371,10 +394,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
       T res[V];
       stage_out(interior_tag, t, minus, row, gc0, cols_inner, res);
       if (t == TS - 1) {
-        if (lane_store && (STEADY || (row >= i0 && row < i1))) store_vec(out_last, row, gc0, res);
+        if (lane_store && (STEADY || (row >= i0 && row < i1)))
+          store_vec(out_last, row, gc0, res, true);
       } else {
         if (t == TS - 2 && lane_store && row >= i0 && row < i1)
-          store_vec(out_prev, row, gc0, res);
+          store_vec(out_prev, row, gc0, res, false);
         admit(t + 1, res);
       }
     }

@@ -95,31 +95,40 @@ class VirtualSlabs:
 
     def __init__(self, scheme, n: int, lam: float, P: int, ring: int | None = None,
                  dtype: str = "f64", arith: str = "ref", c: float = 1.0,
-                 transport: str = "copy"):
+                 transport: str = "copy", tsteps: int = 1):
         if transport not in ("copy", "kernel"):
             raise ValueError(f"transport must be 'copy' or 'kernel', got {transport!r}")
+        if tsteps not in (1, 2, 4):
+            raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
         self.transport = transport
+        self.T = int(tsteps)
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         self.n, self.lam, self.P = int(n), float(lam), int(P)
         self.tau = self.lam / self.n / c
         R = self.spec.radius
+        self.R = R
         self.ring = R if ring is None else int(ring)
         grows = self.n + 1
-        self.plans = [SlabPlan.build(grows, P, p, R, periodic=False) for p in range(P)]
-        self.grids = [nat.make_slab_grid(grows, grows, pl.row0, pl.rows, max(2, R), self.ring,
+        H = R * self.T
+        self.plans = [SlabPlan.build(grows, P, p, H, periodic=False) for p in range(P)]
+        self.grids = [nat.make_slab_grid(grows, grows, pl.row0, pl.rows, max(2, H), self.ring,
                                          "dirichlet", dtype, arith) for pl in self.plans]
-        self.levels = [[nat.Level(g) for _ in range(3)] for g in self.grids]
+        self.levels = [[nat.Level(g) for _ in range(3 if self.T == 1 else 4)]
+                       for g in self.grids]
+        self.previous = None
         self.t_u = nat.make_table(evaluate_table(self.spec.first_u, self.lam))
         self.t_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
         self.t_two = nat.make_table(evaluate_table(self.spec.two_step, self.lam))
         self.newest = None
 
-    def _exchange(self, idx: int):
+    def _exchange(self, idx: int, count: int | None = None):
         for p, pl in enumerate(self.plans):
-            for peer, first, count in pl.sends:
-                dst_first = -count if peer > p else self.plans[peer].rows
-                rows_view(self.levels[peer][idx], dst_first, count).copy_(
-                    rows_view(self.levels[p][idx], first, count))
+            for peer, first, halo in pl.sends:
+                k = halo if count is None else count
+                src_first = 0 if first == 0 else pl.rows - k
+                dst_first = -k if peer > p else self.plans[peer].rows
+                rows_view(self.levels[peer][idx], dst_first, k).copy_(
+                    rows_view(self.levels[p][idx], src_first, k))
 
     def load_initial(self, u0: np.ndarray, v0: np.ndarray):
         for pl, lv in zip(self.plans, self.levels):
@@ -132,12 +141,42 @@ class VirtualSlabs:
         for g, lv in zip(self.grids, self.levels):
             nat.first_step(g, lv[1], lv[0], lv[2], self.t_u, self.t_v, self.tau)
         self._exchange(2)
-        self.newest = 2
+        self.newest, self.previous = 2, 1
+
+    def _march_blocked(self, nsteps: int):
+        """Fused passes of T updates; halos of both output levels by device copies or by
+        the fused kernel's own stores into the neighbours' ghost rows."""
+        if nsteps % self.T:
+            raise ValueError(f"nsteps={nsteps} must be a multiple of tsteps={self.T}")
+        T, R = self.T, self.R
+        for _ in range(nsteps // T):
+            cur, prev = self.newest, self.previous
+            f1, f2 = [x for x in range(4) if x not in (cur, prev)]
+            for p, (g, lv) in enumerate(zip(self.grids, self.levels)):
+                if self.transport == "copy":
+                    nat.two_step_tb_rows(g, lv[cur], lv[prev], lv[f1], lv[f2], self.t_two, T, 0,
+                                         g.rows)
+                    continue
+                up = ((self.levels[p - 1][f1].ptr.value, self.levels[p - 1][f2].ptr.value)
+                      if p > 0 else None)
+                dn = ((self.levels[p + 1][f1].ptr.value, self.levels[p + 1][f2].ptr.value)
+                      if p + 1 < self.P else None)
+                up_rows = self.plans[p - 1].rows if p > 0 else 0
+                nat.two_step_tb_halo(g, lv[cur], lv[prev], lv[f1], lv[f2], self.t_two, T, 0,
+                                     g.rows, up, up_rows, dn)
+            if self.transport == "copy":
+                self._exchange(f2, R * T)
+                self._exchange(f1, R * (T - 1))
+            self.newest, self.previous = f2, f1
 
     def march(self, nsteps: int):
+        if self.T > 1:
+            self._march_blocked(nsteps)
+            return
         for _ in range(nsteps):
             cur = self.newest
             nxt, prev = (cur + 1) % 3, (cur + 2) % 3
+            R = self.R
             for p, (g, lv) in enumerate(zip(self.grids, self.levels)):
                 if self.transport == "copy":
                     nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
@@ -148,8 +187,8 @@ class VirtualSlabs:
                 nat.two_step_halo(g, lv[cur], lv[prev], lv[nxt], self.t_two, 0, g.rows, up,
                                   up_rows, dn)
             if self.transport == "copy":
-                self._exchange(nxt)
-            self.newest = nxt
+                self._exchange(nxt, R)
+            self.newest, self.previous = nxt, cur
 
     def field(self) -> np.ndarray:
         return np.concatenate([lv[self.newest].download() for lv in self.levels], axis=0)
@@ -173,8 +212,6 @@ class DistributedSlabs:
             raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
         if tsteps not in (1, 2, 4):
             raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
-        if tsteps > 1 and transport != "nccl":
-            raise ValueError("temporal blocking across slabs uses the nccl transport")
         self.transport = transport
         # Temporal blocking depth T: one pass advances T steps, so the halo is R*T rows of
         # the newest level and R*(T-1) rows of the one before.
@@ -206,7 +243,7 @@ class DistributedSlabs:
 
     # -- p2p transport: neighbours' levels mapped through CUDA IPC ------------------------
     def _open_peers(self):
-        """Exchange IPC handles of the three levels; map the up/down neighbours' levels."""
+        """Exchange IPC handles of the levels; map the up/down neighbours' levels."""
         mine = [nat.ipc_handle(lv.ptr.value) for lv in self.levels]
         allh = [None] * self.P
         self.dist.all_gather_object(allh, (self.plan.rows, mine), group=self.group)
@@ -346,7 +383,7 @@ class DistributedSlabs:
         H = R * T
         if self.P == 1 or rows < 3 * H or not overlap or not c.is_cuda:
             c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, rows)
-            self.exchange(f2, H, f1, R * (T - 1))
+            self.exchange(f2, H, f1, R * (T - 1))   # (p2p slabs too: plain copy here)
         else:
             import torch
 
@@ -354,12 +391,26 @@ class DistributedSlabs:
                 self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
             comm, ev_edge, ev_comm = self._streams
             main = torch.cuda.current_stream()
-            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H)
-            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows)
+            if self.transport == "p2p":
+                # the boundary passes store their rows of both output levels straight into
+                # the neighbours' ghost rows (peer memory); a token orders the next pass
+                pr = self._peer
+                up = (pr["up"][f1], pr["up"][f2]) if pr["up"] else None
+                dn = (pr["dn"][f1], pr["dn"][f2]) if pr["dn"] else None
+                c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H, up,
+                          pr["up_rows"], dn)
+                c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows, up,
+                          pr["up_rows"], dn)
+            else:
+                c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H)
+                c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows)
             ev_edge.record(main)
             with torch.cuda.stream(comm):
                 comm.wait_event(ev_edge)
-                self.exchange(f2, H, f1, R * (T - 1))
+                if self.transport == "p2p":
+                    self._token_exchange()
+                else:
+                    self.exchange(f2, H, f1, R * (T - 1))
                 ev_comm.record(comm)
             c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, H, rows - H)
             main.wait_event(ev_comm)
@@ -405,3 +456,8 @@ class _KernelCompute:
     def tb_rows(self, grid, uk, ukm1, out_prev, out_last, T, lo, hi):
         if hi > lo:
             nat.two_step_tb_rows(grid, uk, ukm1, out_prev, out_last, self.t_two, T, lo, hi)
+
+    def tb_halo(self, grid, uk, ukm1, out_prev, out_last, T, lo, hi, up, up_rows, dn):
+        if hi > lo:
+            nat.two_step_tb_halo(grid, uk, ukm1, out_prev, out_last, self.t_two, T, lo, hi, up,
+                                 up_rows, dn)

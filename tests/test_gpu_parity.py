@@ -220,6 +220,38 @@ def test_row_range_and_virtual_slabs_bitwise(nat, oracle, ps):
             assert same_bits(vs.field(), want), (P, transport)
 
 
+@pytest.mark.parametrize("name,dtype,arith", [("P13", "f64", "ref"), ("P9", "f64", "ref"),
+                                              ("P13", "f32", "native"), ("P5", "f32", "ref")])
+@pytest.mark.parametrize("tsteps", [2, 4])
+def test_virtual_slabs_temporal_blocking_bitwise(oracle, name, dtype, arith, tsteps):
+    """Fused passes across row slabs: halos of both output levels (R*T and R*(T-1) rows)
+    moved by device copies, or stored into the neighbours' ghost rows by the fused kernel
+    itself (ps_two_step_tb_halo) — both equal the single-grid march bit for bit."""
+    from paper_1904_04048_b200.scheme import named_scheme
+    from paper_1904_04048_b200.slab import VirtualSlabs
+
+    n, steps = 601, 4 * tsteps
+    spec = named_scheme(name)
+    lam = 0.4 if spec.radius == 2 else 0.6
+    ring = spec.radius
+    npdt = np.float64 if dtype == "f64" else np.float32
+    rng = np.random.default_rng(11 + tsteps)
+    u0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    v0 = rng.normal(size=(n + 1, n + 1)).astype(npdt)
+    o1 = oracle.first_step(u0, v0, pairs(spec, "first_u", lam), pairs(spec, "first_v", lam),
+                           lam / n, "dirichlet", ring, arith)
+    want, want_prev = oracle.march(o1, u0, pairs(spec, "two_step", lam), steps, "dirichlet",
+                                   ring, arith)
+    for P in (1, 2, 3, 5):
+        for transport in ("copy", "kernel"):
+            vs = VirtualSlabs(spec, n, lam, P, ring=ring, dtype=dtype, arith=arith,
+                              transport=transport, tsteps=tsteps)
+            vs.load_initial(u0, v0)
+            vs.first_step()
+            vs.march(steps)
+            assert same_bits(vs.field(), want), (P, transport)
+
+
 def test_gaussian_initial_data_matches_numpy(oracle):
     from paper_1904_04048_b200.device import Simulation
 
