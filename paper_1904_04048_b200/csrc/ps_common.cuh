@@ -323,14 +323,14 @@ constexpr int tb_ns() {
   return PS_TB_NS > 0 ? PS_TB_NS : 3;
 }
 
-template <typename T, int A, class S, int TS, bool PER>
+template <typename T, int A, class S, int TS, bool PER, bool HALO>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
   constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
-  auto kern = k_two_step_tb<T, A, S, TS, PER, NW, RB, NS>;
+  auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS>;
   static std::once_flag once;
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {
@@ -397,18 +397,29 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   return last_cuda_status();
 }
 
+template <typename T, int A, int TS, class S>
+static ps_status launch_tb_bc(const ps_grid* g, const void* uk, const void* ukm1, void* op,
+                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
+                              cudaStream_t st, bool rev, int rc, const TBHalo& h) {
+  if (g->bc == PS_BC_PERIODIC)
+    return launch_tb<T, A, S, TS, true, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+  if (h.up_prev || h.up_last || h.dn_prev || h.dn_last)
+    return launch_tb<T, A, S, TS, false, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+  return launch_tb<T, A, S, TS, false, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+}
+
 template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
                              cudaStream_t st, bool rev, int rc, const TBHalo& h) {
   if (shape_matches<ShapeP5>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP5, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP5, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    return launch_tb_bc<T, A, TS, ShapeP5>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    return launch_tb_bc<T, A, TS, ShapeP9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeC9>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeC9, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeC9, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    return launch_tb_bc<T, A, TS, ShapeC9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP13>(t))
-    return g->bc == PS_BC_PERIODIC ? launch_tb<T, A, ShapeP13, TS, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h) : launch_tb<T, A, ShapeP13, TS, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    return launch_tb_bc<T, A, TS, ShapeP13>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   return PS_ERR_TABLE;
 }
 

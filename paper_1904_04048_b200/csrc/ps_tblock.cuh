@@ -108,7 +108,10 @@ __host__ __device__ constexpr int row_need(int d) {
   return need;
 }
 
-template <typename T, int A, class S, int TS, bool PER, int NW, int RB, int NS>
+// HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate
+// instance, so the plain pass keeps its store path free of the extra checks: they cost
+// C5 26 % when compiled into every instance)
+template <typename T, int A, class S, int TS, bool PER, bool HALO, int NW, int RB, int NS>
 __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
   constexpr bool NARROW = tb_narrow<T, S, TS>();
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
   // last = true: out_last (halo depth R*TS), else out_prev (depth R*(TS-1))
   auto store_vec = [&](T* base, int row, int gc0, const T* res, bool last) {
     put(base + int64_t(row) * pitch + gc0, gc0, res);
-    if constexpr (!PER) {
+    if constexpr (HALO && !PER) {
       // fused halo delivery: boundary rows also go straight into the neighbours' ghost
       // rows (peer memory over NVLink, ps_two_step_tb_halo)
       void* hu = last ? p.hu_last : p.hu_prev;
