@@ -314,9 +314,20 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #ifndef PS_TB_NS
 #define PS_TB_NS 0
 #endif
-template <typename T, int TS>
+#ifndef PS_TB_VM
+#define PS_TB_VM 0
+#endif
+// 16-byte vectors per lane (TBGeom VM).  Measured (C4, f64 P9 T=4, 40 steps): two vectors
+// per lane in 7 consumer warps (8 warps per SM -> up to 255 registers, no spills) 585 vs
+// 535 GLUP/s for one vector in 11 warps (168 registers); P13 f64 (358 vs 368) and f32
+// (708 vs 1008: spills) stay at one vector.
+template <typename T, class S, int TS>
+constexpr int tb_vm() {
+  return PS_TB_VM > 0 ? PS_TB_VM : ((sizeof(T) == 8 && S::R == 1) ? 2 : 1);
+}
+template <typename T, class S, int TS>
 constexpr int tb_nw() {
-  return PS_TB_NW > 0 ? PS_TB_NW : 11;
+  return PS_TB_NW > 0 ? PS_TB_NW : (tb_vm<T, S, TS>() == 2 ? 7 : 11);
 }
 template <typename T, int TS>
 constexpr int tb_ns() {
@@ -327,10 +338,10 @@ template <typename T, int A, class S, int TS, bool PER, bool HALO>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
-  constexpr int NW = tb_nw<T, TS>(), NS = tb_ns<T, TS>();
+  constexpr int VM = tb_vm<T, S, TS>(), NW = tb_nw<T, S, TS>(), NS = tb_ns<T, TS>();
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
-  using Gm = TBGeom<T, NW, RB, NS, S::R, TS>;
-  auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS>;
+  using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
+  auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM>;
   static std::once_flag once;
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {

@@ -6,7 +6,7 @@
 //
 // Same producer/consumer skeleton as k_two_step_stream (TMA bulk row copies into an
 // mbarrier ring, dynamic tiles).  The difference is in the consumers:
-//   * each WARP is an independent column unit of 32 vectors (32*V columns) whose
+//   * each WARP is an independent column unit of 32 lanes x V values (32*V columns) whose
 //     outputs are valid on the centre WO = 32V - 2HT columns (HT = R*(TS-1) rounded up
 //     to a vector); neighbouring warps overlap by 2HT columns, so no cross-warp exchange
 //     is ever needed — the halo is recomputed instead of communicated;
@@ -47,15 +47,19 @@ struct TBParams {
   float cf[PS_MAX_TAPS];
 };
 
-template <typename T, int NW, int RB, int NS, int R, int TS>
+// VM: 16-byte vectors owned per lane (1 or 2).  Two vectors per lane halve the share of
+// recomputed halo columns (f64 T=4: 64/56 -> 128/120) and give each stage twice the
+// independent add chains per warp, at twice the window registers.
+template <typename T, int NW, int RB, int NS, int R, int TS, int VM = 1>
 struct TBGeom {
-  static constexpr int V = Vec<T>::V;
+  static constexpr int VV = Vec<T>::V;                     // elements per 16-byte vector
+  static constexpr int V = VM * VV;                        // elements owned per lane
   // Column halo per side.  Stage 1 reads true neighbours from shared memory; each later
-  // stage loses R valid columns at each warp edge, so R*(TS-1) (rounded to a vector).
+  // stage loses R valid columns at each warp edge, so R*(TS-1) (rounded to a lane).
   static constexpr int HT = ((R * (TS - 1) + V - 1) / V) * V;
   static constexpr int WO = 32 * V - 2 * HT;              // valid output columns per warp
   static constexpr int W = NW * WO;                        // output columns per block strip
-  static constexpr int LU = W + 2 * HT + 2 * V;            // u^k row slot (extra vec each side)
+  static constexpr int LU = W + 2 * HT + 2 * VV;           // u^k row slot (extra vec each side)
   static constexpr int LK = W + 2 * HT;                    // u^{k-1} row slot
   static constexpr size_t smem_bytes =
       size_t(NS) * RB * (LU + LK) * sizeof(T) + 2 * NS * sizeof(uint64_t) + 2 * NS * sizeof(int);
@@ -111,15 +115,15 @@ __host__ __device__ constexpr int row_need(int d) {
 // HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate
 // instance, so the plain pass keeps its store path free of the extra checks: they cost
 // C5 26 % when compiled into every instance)
-template <typename T, int A, class S, int TS, bool PER, bool HALO, int NW, int RB, int NS>
+template <typename T, int A, class S, int TS, bool PER, bool HALO, int NW, int RB, int NS, int VM>
 __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
   constexpr bool NARROW = tb_narrow<T, S, TS>();
   constexpr int R = S::R;
-  using G = TBGeom<T, NW, RB, NS, R, TS>;
-  constexpr int V = G::V, HT = G::HT, WO = G::WO, W = G::W, LU = G::LU, LK = G::LK;
+  using G = TBGeom<T, NW, RB, NS, R, TS, VM>;
+  constexpr int V = G::V, VV = G::VV, HT = G::HT, WO = G::WO, W = G::W, LU = G::LU, LK = G::LK;
   constexpr int WC = V + 2 * R;  // window row: R left | V own | R right
-  static_assert(R <= V, "neighbour vector must cover the radius");
+  static_assert(R <= VV, "neighbour vector must cover the radius");
   using Ar = Arith<T, A>;
   using acc_t = typename Ar::acc_t;
   using coef_t = typename Ar::coef_t;
@@ -168,10 +172,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
         const int i0 = p.rlo + chunk * p.rc;
         const int i1 = min(i0 + p.rc, p.rhi);
         const int j0 = strip * W;
-        // columns: u^k from j0-HT-V, u^{k-1} from j0-HT; clamp to the allocation row
-        const int cu0 = j0 - HT - V, ck0 = j0 - HT;
-        const int nu = max(0, min(LU, p.cmax - cu0)) / V * V;
-        const int nk = max(0, min(LK, p.cmax - ck0)) / V * V;
+        // columns: u^k from j0-HT-VV, u^{k-1} from j0-HT; clamp to the allocation row
+        const int cu0 = j0 - HT - VV, ck0 = j0 - HT;
+        const int nu = max(0, min(LU, p.cmax - cu0)) / VV * VV;
+        const int nk = max(0, min(LK, p.cmax - ck0)) / VV * VV;
         const uint32_t ub = uint32_t(nu) * sizeof(T), kb = uint32_t(nk) * sizeof(T);
         const int ne = (i1 - i0) + NE_EXTRA;
         for (int mlo = 0; mlo < ne; mlo += RB, ++g) {
@@ -234,8 +238,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
 #pragma unroll
       for (int x = 0; x < WC; ++x) win[t][r][x] = T(0);
 
-  const int xo = V + warp * WO + lane * V;  // own vector's column in the u^k slot
-  const int xk = warp * WO + lane * V;      // own vector's column in the u^{k-1} slot
+  const int xo = VV + warp * WO + lane * V;  // own values' first column in the u^k slot
+  const int xk = warp * WO + lane * V;       // own values' first column in the u^{k-1} slot
   const bool lane_out = (lane * V >= HT) && (lane * V + V <= HT + WO);
 
   const int gc_lane = warp * WO + lane * V - HT;  // own column relative to the strip start
@@ -315,13 +319,15 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     for (int r = 0; r < 2 * R; ++r)
 #pragma unroll
       for (int x = 0; x < WC; ++x) win[0][r][x] = win[0][r + 1][x];
-    T l[V], o[V], rr[V];
-    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - V), l);
-    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo), o);
+    T l[VV], o[V], rr[VV];
+    Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - VV), l);
+#pragma unroll
+    for (int m = 0; m < VM; ++m)
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + m * VV), o + m * VV);
     Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + V), rr);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      win[0][2 * R][q] = l[V - R + q];
+      win[0][2 * R][q] = l[VV - R + q];
       win[0][2 * R][R + V + q] = rr[q];
     }
 #pragma unroll
@@ -330,7 +336,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
 
   auto put = [&](T* dst, int gc0, const T* res) {
     if (gc0 + V <= p.cols) {
-      *reinterpret_cast<vec_t*>(dst) = Vec<T>::pack(res);
+#pragma unroll
+      for (int m = 0; m < VM; ++m)
+        reinterpret_cast<vec_t*>(dst)[m] = Vec<T>::pack(res + m * VV);
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v)
@@ -389,7 +397,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
       const int row = e - (t + 1) * R;
       T minus[V];
       if (t == 0) {
-        Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + xk), minus);
+#pragma unroll
+        for (int m = 0; m < VM; ++m)
+          Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + xk + m * VV), minus + m * VV);
       } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) minus[v] = win[t - 1][0][R + v];

@@ -361,7 +361,7 @@ def test_config4_full_size_slab_check(oracle):
 @pytest.mark.parametrize("name,radius", SHAPES)
 @pytest.mark.parametrize("dtype,arith", [("f64", "ref"), ("f32", "ref"), ("f32", "native")])
 @pytest.mark.parametrize("tsteps", [2, 4])
-@pytest.mark.parametrize("n", [45, 700])
+@pytest.mark.parametrize("n", [45, 700, 2100])  # 2100: several column strips at every geometry
 @pytest.mark.parametrize("bc", ["dirichlet", "periodic"])
 def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps, n, bc, oracle):
     """T fused steps per pass equal T single steps bit for bit (incl. a remainder step,

@@ -10,15 +10,19 @@
 # the TS stages of a step are independent: 4x the add chains per warp, bitwise correct) needs
 # ~200 registers and ran 452 (7 warps) / 430 (11 warps, spills).  Register caps: a 9-warp block can use at most
 # 168 registers per thread (3 warps share one SM sub-partition's 16K registers).
+# Session 4: two 16-B vectors per lane in 7 consumer warps (PS_TB_VM=2, 8 warps -> 228
+# registers, no spills): C4 535 -> 558-585; with it, starting the sum at the first product
+# and fixing -0.0 on p0 only (off the add chain) still lost (540); f32 P13 T=4 with two
+# vectors per lane: 718 (narrow windows) / 634 (wide) vs 1009 -- f32 and P13 keep one vector.
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
-  [ns2]="-DPS_TB_NS=2"
-  [ns4]="-DPS_TB_NS=4"
-  [rb2]="-DPS_TB_RB=2"
+  [skip0]="-DPS_TB_SKIP0=1"
+  [f32vm2w]="-DPS_TB_VM=2 -DPS_TB_NW=7 -DPS_TB_NARROW=0"
+  [f32vm2n]="-DPS_TB_VM=2 -DPS_TB_NW=7"
 )
 if [ "${MODE:-build}" = build ]; then
   make -s -j4 paper_1904_04048_b200/libps.so
@@ -32,7 +36,7 @@ if [ "${MODE:-build}" = build ]; then
   wait
 else
   mkdir -p gpurun_out
-  for rep in 1 2; do
+  for rep in ${REPS:-1 2}; do
   for v in "${!VARIANTS[@]}"; do
     for ct in ${CONFIGS:-C4:4 C5:4 C2:4 C3:2 C3f32:4}; do
       c=${ct%%:*}; t=${ct##*:}
