@@ -319,15 +319,17 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #endif
 // 16-byte vectors per lane (TBGeom VM).  Measured (C4, f64 P9 T=4, 40 steps): two vectors
 // per lane in 7 consumer warps (8 warps per SM -> up to 255 registers, no spills) 585 vs
-// 535 GLUP/s for one vector in 11 warps (168 registers); P13 f64 (358 vs 368) and f32
-// (708 vs 1008: spills) stay at one vector.
-template <typename T, class S, int TS>
+// 535 GLUP/s for one vector in 11 warps (168 registers); P13 f64 (358 vs 368), f32 (708
+// vs 1008: spills) and periodic grids (C2: 251 vs 324) stay at one vector.  Folding the
+// producer into consumer warp 0 (8 consumer warps, 2 per sub-partition) lost everywhere
+// (C4 528, C5 801).
+template <typename T, class S, int TS, bool PER>
 constexpr int tb_vm() {
-  return PS_TB_VM > 0 ? PS_TB_VM : ((sizeof(T) == 8 && S::R == 1) ? 2 : 1);
+  return PS_TB_VM > 0 ? PS_TB_VM : ((sizeof(T) == 8 && S::R == 1 && !PER) ? 2 : 1);
 }
-template <typename T, class S, int TS>
+template <typename T, class S, int TS, bool PER>
 constexpr int tb_nw() {
-  return PS_TB_NW > 0 ? PS_TB_NW : (tb_vm<T, S, TS>() == 2 ? 7 : 11);
+  return PS_TB_NW > 0 ? PS_TB_NW : (tb_vm<T, S, TS, PER>() == 2 ? 7 : 11);
 }
 template <typename T, int TS>
 constexpr int tb_ns() {
@@ -338,7 +340,8 @@ template <typename T, int A, class S, int TS, bool PER, bool HALO>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
-  constexpr int VM = tb_vm<T, S, TS>(), NW = tb_nw<T, S, TS>(), NS = tb_ns<T, TS>();
+  constexpr int VM = tb_vm<T, S, TS, PER>(), NW = tb_nw<T, S, TS, PER>(), NS = tb_ns<T, TS>();
+  constexpr int NT = (NW + 1) * 32;  // threads per block: consumers + the producer warp
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM>;
@@ -346,7 +349,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, (NW + 1) * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, NT,
                                                   Gm::smem_bytes);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   });
@@ -402,7 +405,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
   const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
-  if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
+  if (launch_pdl(kern, grid, NT, Gm::smem_bytes, st, p, slot) != cudaSuccess)
     return PS_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return last_cuda_status();

@@ -101,6 +101,27 @@ __host__ __device__ constexpr bool tb_narrow() {
   return PS_TB_NARROW >= 0 ? PS_TB_NARROW != 0 : (sizeof(T) == 4 && TS == 4);
 }
 
+// VM 16-byte vector stores of res[0 .. VM*16/sizeof(T)) to dst, predicated on `pred`
+// (an @P STG, not a branch).  Interior tiles only: dst is in bounds and 16-B aligned.
+template <typename T, int VM>
+__device__ __forceinline__ void st_pred(T* dst, const T* res, bool pred) {
+#pragma unroll
+  for (int m = 0; m < VM; ++m) {
+    if constexpr (sizeof(T) == 8) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t"
+          "@p st.global.v2.f64 [%1], {%2, %3};\n\t}" ::"r"(int(pred)),
+          "l"(dst + 2 * m), "d"(double(res[2 * m])), "d"(double(res[2 * m + 1])));
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %0, 0;\n\t"
+          "@p st.global.v4.f32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"(int(pred)),
+          "l"(dst + 4 * m), "f"(float(res[4 * m])), "f"(float(res[4 * m + 1])),
+          "f"(float(res[4 * m + 2])), "f"(float(res[4 * m + 3])));
+    }
+  }
+}
+
 // Largest |q2| among the taps of row offset d (how many neighbour columns it reads).
 template <class S>
 __host__ __device__ constexpr int row_need(int d) {
@@ -157,64 +178,81 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
   const int64_t pitch = p.pitch;
   constexpr int NE_EXTRA = 2 * R * TS;  // u^k rows beyond the chunk (both sides)
 
-  if (warp == NW) {
-    if (lane == 0) {
-      const uint64_t pol_uk = l2_policy_evict_normal();
-      const uint64_t pol_km = l2_policy_evict_first();
-      uint32_t g = 0;
-      int tile = blockIdx.x;
-      while (tile < p.ntiles) {
-        // reversed launches walk the tiles bottom-up, so the rows the previous launch
-        // wrote last (still in L2) are read first
-        const int tid = p.reverse ? p.ntiles - 1 - tile : tile;
-        const int chunk = tid / p.nstrips;
-        const int strip = tid - chunk * p.nstrips;
-        const int i0 = p.rlo + chunk * p.rc;
-        const int i1 = min(i0 + p.rc, p.rhi);
-        const int j0 = strip * W;
-        // columns: u^k from j0-HT-VV, u^{k-1} from j0-HT; clamp to the allocation row
-        const int cu0 = j0 - HT - VV, ck0 = j0 - HT;
-        const int nu = max(0, min(LU, p.cmax - cu0)) / VV * VV;
-        const int nk = max(0, min(LK, p.cmax - ck0)) / VV * VV;
-        const uint32_t ub = uint32_t(nu) * sizeof(T), kb = uint32_t(nk) * sizeof(T);
-        const int ne = (i1 - i0) + NE_EXTRA;
-        for (int mlo = 0; mlo < ne; mlo += RB, ++g) {
-          const uint32_t s = g % NS;
-          const uint32_t k = g / NS;
-          if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
-          s_tile[s] = tid;
-          s_mlo[s] = mlo;
-          const int mhi = min(mlo + RB, ne);
-          uint32_t bytes = 0;
-          for (int m = mlo; m < mhi; ++m) {
-            const int e = i0 - R * TS + m;
-            if (e >= p.gmin && e < p.gmax) bytes += ub;
-            const int ek = e - R;
-            if (m >= 2 * R && ek >= p.gmin && ek < p.gmax) bytes += kb;
-          }
-          mbar_arrive_expect_tx(&full[s], bytes);
-          for (int m = mlo; m < mhi; ++m) {
-            const int e = i0 - R * TS + m;
-            if (e >= p.gmin && e < p.gmax && ub)
-              tma_load_1d(s_uk + (s * RB + (m - mlo)) * LU, uk + int64_t(e) * pitch + cu0, ub,
-                          &full[s], pol_uk);
-            const int ek = e - R;
-            if (m >= 2 * R && ek >= p.gmin && ek < p.gmax && kb)
-              tma_load_1d(s_km + (s * RB + (m - mlo)) * LK, ukm1 + int64_t(ek) * pitch + ck0, kb,
-                          &full[s], pol_km);
-          }
-        }
-        tile = int(gridDim.x + atomicAdd(&g_tile_next[slot], 1u));
-      }
-      const uint32_t s = g % NS;
-      const uint32_t k = g / NS;
-      if (k > 0) mbar_wait(&empty[s], (k - 1) & 1);
+  // ---------------- producer (one thread) ------------------------------------
+  // Issues pipeline slot P.g: the TMA row copies of rows [P.mlo, P.mlo + RB) of tile P.tile
+  // (or the end sentinel once the tiles are exhausted).  The caller has waited until every
+  // consumer warp released that ring stage.  Runs on the producer warp's lane 0.
+  struct Prod {
+    uint32_t g;
+    int tile, mlo;
+    bool done;
+  };
+  auto prod_issue = [&](Prod& P) {
+    const uint32_t s = P.g % NS;
+    if (P.tile >= p.ntiles) {
       s_tile[s] = -1;
       mbar_arrive(&full[s]);
+      P.done = true;
       __threadfence();
       if (atomicAdd(&g_tile_done[slot], 1u) == gridDim.x - 1) {
         g_tile_next[slot] = 0;
         g_tile_done[slot] = 0;
+      }
+      return;
+    }
+    // reversed launches walk the tiles bottom-up, so the rows the previous launch wrote
+    // last (still in L2) are read first
+    const int tid = p.reverse ? p.ntiles - 1 - P.tile : P.tile;
+    const int chunk = tid / p.nstrips;
+    const int strip = tid - chunk * p.nstrips;
+    const int i0 = p.rlo + chunk * p.rc;
+    const int i1 = min(i0 + p.rc, p.rhi);
+    const int j0 = strip * W;
+    // columns: u^k from j0-HT-VV, u^{k-1} from j0-HT; clamp to the allocation row
+    const int cu0 = j0 - HT - VV, ck0 = j0 - HT;
+    const int nu = max(0, min(LU, p.cmax - cu0)) / VV * VV;
+    const int nk = max(0, min(LK, p.cmax - ck0)) / VV * VV;
+    const uint32_t ub = uint32_t(nu) * sizeof(T), kb = uint32_t(nk) * sizeof(T);
+    const int ne = (i1 - i0) + NE_EXTRA;
+    const int mlo = P.mlo;
+    s_tile[s] = tid;
+    s_mlo[s] = mlo;
+    const int mhi = min(mlo + RB, ne);
+    uint32_t bytes = 0;
+    for (int m = mlo; m < mhi; ++m) {
+      const int e = i0 - R * TS + m;
+      if (e >= p.gmin && e < p.gmax) bytes += ub;
+      const int ek = e - R;
+      if (m >= 2 * R && ek >= p.gmin && ek < p.gmax) bytes += kb;
+    }
+    mbar_arrive_expect_tx(&full[s], bytes);
+    const uint64_t pol_uk = l2_policy_evict_normal();
+    const uint64_t pol_km = l2_policy_evict_first();
+    for (int m = mlo; m < mhi; ++m) {
+      const int e = i0 - R * TS + m;
+      if (e >= p.gmin && e < p.gmax && ub)
+        tma_load_1d(s_uk + (s * RB + (m - mlo)) * LU, uk + int64_t(e) * pitch + cu0, ub,
+                    &full[s], pol_uk);
+      const int ek = e - R;
+      if (m >= 2 * R && ek >= p.gmin && ek < p.gmax && kb)
+        tma_load_1d(s_km + (s * RB + (m - mlo)) * LK, ukm1 + int64_t(ek) * pitch + ck0, kb,
+                    &full[s], pol_km);
+    }
+    ++P.g;
+    P.mlo += RB;
+    if (P.mlo >= ne) {
+      P.mlo = 0;
+      P.tile = int(gridDim.x + atomicAdd(&g_tile_next[slot], 1u));
+    }
+  };
+  Prod P{0u, int(blockIdx.x), 0, false};
+
+  if (warp == NW) {
+    if (lane == 0) {
+      while (!P.done) {
+        const uint32_t k = P.g / NS;
+        if (k > 0) mbar_wait(&empty[P.g % NS], (k - 1) & 1);
+        prod_issue(P);
       }
     }
     return;
@@ -406,12 +444,23 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
       }
       T res[V];
       stage_out(interior_tag, t, minus, row, gc0, cols_inner, res);
+      // steady interior slots of a plain pass store with predicated vector stores: no
+      // branch (and no reconvergence point) splits the unrolled rows, so the scheduler
+      // can overlap one stage's dependent add chain with the next row's products
+      constexpr bool PRED_ST = STEADY && decltype(interior_tag)::value && !PER && !HALO;
       if (t == TS - 1) {
-        if (lane_store && (STEADY || (row >= i0 && row < i1)))
+        if constexpr (PRED_ST)
+          st_pred<T, VM>(out_last + int64_t(row) * pitch + gc0, res, lane_store);
+        else if (lane_store && (STEADY || (row >= i0 && row < i1)))
           store_vec(out_last, row, gc0, res, true);
       } else {
-        if (t == TS - 2 && lane_store && row >= i0 && row < i1)
-          store_vec(out_prev, row, gc0, res, false);
+        if (t == TS - 2) {
+          if constexpr (PRED_ST)
+            st_pred<T, VM>(out_prev + int64_t(row) * pitch + gc0, res,
+                           lane_store && row >= i0 && row < i1);
+          else if (lane_store && row >= i0 && row < i1)
+            store_vec(out_prev, row, gc0, res, false);
+        }
         admit(t + 1, res);
       }
     }
@@ -421,6 +470,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
     const uint32_t s = g % NS;
     const uint32_t k = g / NS;
     mbar_wait(&full[s], k & 1);
+    __syncwarp();  // converged from here on: the shuffles need no divergence checks
     const int tile = s_tile[s];
     if (tile < 0) break;
     const int mlo = s_mlo[s];

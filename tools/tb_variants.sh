@@ -20,9 +20,7 @@ NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcomp
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
-  [skip0]="-DPS_TB_SKIP0=1"
-  [f32vm2w]="-DPS_TB_VM=2 -DPS_TB_NW=7 -DPS_TB_NARROW=0"
-  [f32vm2n]="-DPS_TB_VM=2 -DPS_TB_NW=7"
+
 )
 if [ "${MODE:-build}" = build ]; then
   make -s -j4 paper_1904_04048_b200/libps.so
