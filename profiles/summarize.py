@@ -27,7 +27,15 @@ KEYS = [
     "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
     "smsp__inst_executed.sum", "sm__cycles_active.avg", "sm__cycles_elapsed.avg",
     "sm__cycles_elapsed.avg.per_second", "lts__t_sector_hit_rate.pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.min.pct_of_peak_sustained_active",
+    "smsp__issue_active.max.pct_of_peak_sustained_active",
 ]
+STALL = ("smsp__average_warps_issue_stalled_", "_per_issue_active.ratio")
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0,
@@ -101,6 +109,15 @@ def main():
                 lines.append(f"dram GB/s = {traffic / dur / 1e9:.1f}   "
                              f"algorithmic GB/s (ncu duration) = "
                              f"{(a.bytes_per_launch or 0) / dur / 1e9:.1f}")
+        stalls = []
+        for k, (v, u) in d.items():
+            if k.startswith(STALL[0]) and k.endswith(STALL[1]):
+                x = to_float(v, u)
+                if x is not None and x >= 0.05:
+                    stalls.append((x, k[len(STALL[0]):-len(STALL[1])]))
+        if stalls:
+            lines.append("stalls per issued instruction: " + ", ".join(
+                f"{n} {x:.2f}" for x, n in sorted(stalls, reverse=True)))
         lines.append("")
     lines.append("## warp state / stalls")
     lines.extend(stall_reasons(a.report))

@@ -14,13 +14,15 @@
 # registers, no spills): C4 535 -> 558-585; with it, starting the sum at the first product
 # and fixing -0.0 on p0 only (off the add chain) still lost (540); f32 P13 T=4 with two
 # vectors per lane: 718 (narrow windows) / 634 (wide) vs 1009 -- f32 and P13 keep one vector.
+# The producer warp leaves one SM sub-partition with a consumer warp fewer; removing it
+# lost both ways: folded into consumer warp 0 (C4 528, C5 801) and as warp-private
+# pipelines, each warp issuing its own copies into its own ring (C4 524, C5 720, C3 274).
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
-
 )
 if [ "${MODE:-build}" = build ]; then
   make -s -j4 paper_1904_04048_b200/libps.so
