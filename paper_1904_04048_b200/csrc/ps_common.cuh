@@ -327,9 +327,28 @@ template <typename T, class S, int TS, bool PER>
 constexpr int tb_vm() {
   return PS_TB_VM > 0 ? PS_TB_VM : ((sizeof(T) == 8 && S::R == 1 && !PER) ? 2 : 1);
 }
+#ifndef PS_TB_WGS
+#define PS_TB_WGS -1
+#endif
+// warpgroup-specialised block (k_two_step_tb WGS).  Measured (40 steps): C4 616-625 vs
+// 579-600 GLUP/s for 7 consumers + a producer warp (200-step bench: 593 vs 564); f32 with
+// 12 consumers (160 registers): C5 1036 -> 1052, C3 f32 804 -> 826; P13 f64 unchanged
+// (370-376), periodic C2 slower (321 -> 291), so those keep 11 consumers + a producer.
+#ifndef PS_TB_WGS1
+#define PS_TB_WGS1 -1  // one-vector geometries: 1 = always, 0 = never, -1 = f32 Dirichlet
+#endif
+template <typename T, class S, int TS, bool PER>
+constexpr bool tb_wgs() {
+  return PS_TB_WGS >= 0 ? PS_TB_WGS != 0
+         : tb_vm<T, S, TS, PER>() == 2
+             ? true
+             : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0 : (sizeof(T) == 4 && !PER));
+}
 template <typename T, class S, int TS, bool PER>
 constexpr int tb_nw() {
-  return PS_TB_NW > 0 ? PS_TB_NW : (tb_vm<T, S, TS, PER>() == 2 ? 7 : 11);
+  return tb_wgs<T, S, TS, PER>() ? (tb_vm<T, S, TS, PER>() == 2 ? 8 : 12)
+         : PS_TB_NW > 0          ? PS_TB_NW
+                                 : (tb_vm<T, S, TS, PER>() == 2 ? 7 : 11);
 }
 template <typename T, int TS>
 constexpr int tb_ns() {
@@ -341,10 +360,11 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
   constexpr int VM = tb_vm<T, S, TS, PER>(), NW = tb_nw<T, S, TS, PER>(), NS = tb_ns<T, TS>();
-  constexpr int NT = (NW + 1) * 32;  // threads per block: consumers + the producer warp
+  constexpr bool WGS = tb_wgs<T, S, TS, PER>();
+  constexpr int NT = (NW + (WGS ? 4 : 1)) * 32;  // threads per block (consumers + producer)
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
-  auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM>;
+  auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
   static std::once_flag once;
   static int blocks_per_sm = 1;
   std::call_once(once, [&] {

@@ -136,9 +136,20 @@ __host__ __device__ constexpr int row_need(int d) {
 // HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate
 // instance, so the plain pass keeps its store path free of the extra checks: they cost
 // C5 26 % when compiled into every instance)
-template <typename T, int A, class S, int TS, bool PER, bool HALO, int NW, int RB, int NS, int VM>
-__global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
+// WGS (warpgroup specialisation): warpgroup 0 hands its registers to the others
+// (setmaxnreg) and its warp 0 is the producer; the NW consumer warps (NW = 8 or 12) fill
+// whole warpgroups, so every SM sub-partition runs the same number of consumers (with a
+// single producer warp, 7 or 11 consumers leave one sub-partition a consumer short).
+template <int NW>
+struct WgsRegs {
+  static constexpr int producer = NW == 8 ? 40 : 32;
+  static constexpr int consumer = (65536 - 128 * producer) / (NW * 32) / 8 * 8;
+};
+template <typename T, int A, class S, int TS, bool PER, bool HALO, int NW, int RB, int NS, int VM,
+          bool WGS>
+__global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, PER>()))
     k_two_step_tb(const __grid_constant__ TBParams p, const int slot) {
+  static_assert(!WGS || NW % 4 == 0, "warpgroup specialisation: whole consumer warpgroups");
   constexpr bool NARROW = tb_narrow<T, S, TS>();
   constexpr int R = S::R;
   using G = TBGeom<T, NW, RB, NS, R, TS, VM>;
@@ -247,8 +258,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
   };
   Prod P{0u, int(blockIdx.x), 0, false};
 
-  if (warp == NW) {
-    if (lane == 0) {
+  if (WGS ? (warp < 4) : (warp == NW)) {
+    if constexpr (WGS)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(WgsRegs<NW>::producer) : "memory");
+    if ((!WGS || warp == 0) && lane == 0) {
       while (!P.done) {
         const uint32_t k = P.g / NS;
         if (k > 0) mbar_wait(&empty[P.g % NS], (k - 1) & 1);
@@ -259,6 +272,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
   }
 
   // ---------------- consumers ------------------------------------------------
+  if constexpr (WGS)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(WgsRegs<NW>::consumer) : "memory");
+  const int cw = WGS ? warp - 4 : warp;  // consumer warp index
   coef_t c[S::N];
 #pragma unroll
   for (int s = 0; s < S::N; ++s) {
@@ -276,11 +292,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, (tb_minb<T, S, TS, PER>()))
 #pragma unroll
       for (int x = 0; x < WC; ++x) win[t][r][x] = T(0);
 
-  const int xo = VV + warp * WO + lane * V;  // own values' first column in the u^k slot
-  const int xk = warp * WO + lane * V;       // own values' first column in the u^{k-1} slot
+  const int xo = VV + cw * WO + lane * V;  // own values' first column in the u^k slot
+  const int xk = cw * WO + lane * V;       // own values' first column in the u^{k-1} slot
   const bool lane_out = (lane * V >= HT) && (lane * V + V <= HT + WO);
 
-  const int gc_lane = warp * WO + lane * V - HT;  // own column relative to the strip start
+  const int gc_lane = cw * WO + lane * V - HT;  // own column relative to the strip start
 
   auto stage_out = [&](auto interior_tag, int t, const T* minus, int row, int gc0,
                        bool cols_inner, T* res) {

@@ -17,12 +17,17 @@
 # The producer warp leaves one SM sub-partition with a consumer warp fewer; removing it
 # lost both ways: folded into consumer warp 0 (C4 528, C5 801) and as warp-private
 # pipelines, each warp issuing its own copies into its own ring (C4 524, C5 720, C3 274).
+# What worked: warpgroup specialisation (setmaxnreg): warpgroup 0 shrinks to 40/32
+# registers and its warp 0 produces, 8 (two-vector) or 12 (f32) consumer warps grow to
+# 232/160 -- every sub-partition gets the same number of consumers: C4 579-600 -> 616-625,
+# C5 1036 -> 1052, C3 f32 804 -> 826 (P13 f64 flat, periodic C2 291 vs 321: not used there).
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
+
 )
 if [ "${MODE:-build}" = build ]; then
   make -s -j4 paper_1904_04048_b200/libps.so
