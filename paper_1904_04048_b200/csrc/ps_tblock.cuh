@@ -463,7 +463,8 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
       // steady interior slots of a plain pass store with predicated vector stores: no
       // branch (and no reconvergence point) splits the unrolled rows, so the scheduler
       // can overlap one stage's dependent add chain with the next row's products
-      constexpr bool PRED_ST = STEADY && decltype(interior_tag)::value && !PER && !HALO;
+      // (periodic: interior = off the wrap-around image bands, so no image stores either)
+      constexpr bool PRED_ST = STEADY && decltype(interior_tag)::value && !HALO;
       if (t == TS - 1) {
         if constexpr (PRED_ST)
           st_pred<T, VM>(out_last + int64_t(row) * pitch + gc0, res, lane_store);
@@ -504,8 +505,10 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
     const bool steady = mlo >= 2 * R * TS && mlo + RB <= ne;
     // every stage output row of this slot lies in [row0+rmin, row0+rmax]
     const int rmin = i0 - R * TS + mlo - TS * R, rmax = i0 - R * TS + mlo + RB - 1 - R;
-    const bool interior = cols_inner && (p.row0 + rmin >= p.ring) &&
-                          (p.row0 + rmax < p.grows - p.ring);
+    constexpr int D = R * TS;  // periodic: depth of the image bands each pass rewrites
+    const bool interior =
+        PER ? ((j0 - HT >= D) && (j0 + W + HT <= p.cols - D) && (rmin >= D) && (rmax < p.rows - D))
+            : cols_inner && (p.row0 + rmin >= p.ring) && (p.row0 + rmax < p.grows - p.ring);
     if (steady && interior) {
 #pragma unroll
       for (int mm = 0; mm < RB; ++mm)

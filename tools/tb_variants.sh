@@ -27,6 +27,8 @@ NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcomp
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
+  [vm2]="-DPS_TB_VM=2"
+  [wgs1]="-DPS_TB_WGS1=1"
 
 )
 if [ "${MODE:-build}" = build ]; then
