@@ -309,7 +309,7 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #define PS_TB_NW 0
 #endif
 #ifndef PS_TB_RB
-#define PS_TB_RB 0  // 0: 2R+1 rows per stage, so a stage is one full window rotation
+#define PS_TB_RB 0  // 0: per radius (launch_tb)
 #endif
 #ifndef PS_TB_NS
 #define PS_TB_NS 0
@@ -362,7 +362,10 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   constexpr int VM = tb_vm<T, S, TS, PER>(), NW = tb_nw<T, S, TS, PER>(), NS = tb_ns<T, TS>();
   constexpr bool WGS = tb_wgs<T, S, TS, PER>();
   constexpr int NT = (NW + (WGS ? 4 : 1)) * 32;  // threads per block (consumers + producer)
-  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : 2 * S::R + 1;
+  // rows per pipeline slot: one window rotation (2R+1) for radius 1; radius 2 takes 6
+  // (measured: C5 1052 -> 1080, C3 f32 827 -> 837 GLUP/s; fewer ring waits per row, and
+  // 8 or 10 rows no longer fit the shared memory)
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
   static std::once_flag once;

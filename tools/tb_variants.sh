@@ -21,14 +21,16 @@
 # registers and its warp 0 produces, 8 (two-vector) or 12 (f32) consumer warps grow to
 # 232/160 -- every sub-partition gets the same number of consumers: C4 579-600 -> 616-625,
 # C5 1036 -> 1052, C3 f32 804 -> 826 (P13 f64 flat, periodic C2 291 vs 321: not used there).
+# Session 5: 6 rows per pipeline slot for radius 2 (PS_TB_RB=6): C5 1052 -> 1080, C3 f32
+# 827 -> 837 (8 and 10 rows exceed shared memory; radius 1 keeps 3: 6 rows do not fit
+# the two-vector f64 ring); 4 ring stages (PS_TB_NS=4): flat; f64 narrow windows: C3 T=4
+# 319 vs 358 at T=2, C2 323 vs 342.
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
 CSRC=paper_1904_04048_b200/csrc
 declare -A VARIANTS=(
   [cur]=""
-  [vm2]="-DPS_TB_VM=2"
-  [wgs1]="-DPS_TB_WGS1=1"
 
 )
 if [ "${MODE:-build}" = build ]; then
