@@ -24,7 +24,8 @@
 # Session 5: 6 rows per pipeline slot for radius 2 (PS_TB_RB=6): C5 1052 -> 1080, C3 f32
 # 827 -> 837 (8 and 10 rows exceed shared memory; radius 1 keeps 3: 6 rows do not fit
 # the two-vector f64 ring); 4 ring stages (PS_TB_NS=4): flat; f64 narrow windows: C3 T=4
-# 319 vs 358 at T=2, C2 323 vs 342.
+# 319 vs 358 at T=2, C2 323 vs 342.  6 rows for radius 1 (periodic C2: 317 vs 333) and 6 rows
+# in 2 ring stages (C4 584 vs 586-634, C2 324, C5 1038 vs 1079): dropped.
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
