@@ -26,6 +26,9 @@
 # the two-vector f64 ring); 4 ring stages (PS_TB_NS=4): flat; f64 narrow windows: C3 T=4
 # 319 vs 358 at T=2, C2 323 vs 342.  6 rows for radius 1 (periodic C2: 317 vs 333) and 6 rows
 # in 2 ring stages (C4 584 vs 586-634, C2 324, C5 1038 vs 1079): dropped.
+# Radius-2 f32 ring shape at ~equal shared memory (C5 / C3 f32): 6x3 rows 1079 / 840,
+# 4x5 995 / 781, 3x6 938 / 748, 8x2 1076 / 830, 9x2 1078 / 821 -- rows per slot matter
+# (per-slot barrier overhead), ring depth beyond 2 slots of slack does not.
 set -e
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 NV="nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Iinclude"
