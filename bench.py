@@ -9,8 +9,11 @@ see DESIGN.md §Measurement).  One "step" = one two-step update of the whole gri
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1..C5|C3f32]
   python bench.py --impl reference ...   # the reference's CPU path (oracle port)
 
-For N>1 run under torchrun: one process per GPU, row slabs, halo rows over NCCL
-(``scaling: strong`` — the grid is fixed).  Prints ONE JSON line on rank 0.
+For N>1: one process per GPU, row slabs, halo rows over NCCL or in-kernel peer stores
+(``scaling: strong`` — the grid is fixed).  Under torchrun the ranks come from the
+environment; a plain ``python bench.py --gpus N`` re-executes itself under
+``torch.distributed.run`` with N ranks (and fails loudly when fewer GPUs are visible).
+Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -104,56 +107,98 @@ def load_traffic(cfg_name, T=1):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    """SM clock and clock-event reasons sampled through NVML every ~4 ms on a host thread
+    during the timed region (``nvidia-smi -lms`` bottoms out near 100 ms, longer than a
+    20-step region); falls back to ``nvidia-smi -lms 20`` when NVML cannot be loaded."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
+
+    def __init__(self, gpu: str, period_s: float = 0.004):
+        self.gpu, self.period = gpu, period_s
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.thread = self.proc = None
+        self.source = None
+
+    def _nvml_loop(self, nv, h):
+        reasons_fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        try:
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            mx = None
+        while True:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                if mx:
+                    self.mx.append(mx)
+                bits = int(reasons_fn(h))
+                for name, bit in self.BITS.items():
+                    if bits & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            if self.stop.wait(self.period):
+                return
+
+    def _smi_pump(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 2 + len(REASONS):
+                continue
+            try:
+                self.sm.append(float(parts[0]))
+                self.mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for r, v in zip(REASONS, parts[2:]):
+                if v.lower() == "active":
+                    self.reasons.add(r)
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = (nv.nvmlDeviceGetHandleByUUID(self.gpu) if self.gpu.startswith("GPU-")
+                 else nv.nvmlDeviceGetHandleByIndex(int(self.gpu)))
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.source = f"NVML, {self.period * 1e3:.0f} ms period"
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         q = "clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._pump, daemon=True)
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20",
+                 "-i", self.gpu], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._smi_pump, daemon=True)
+            self.source = "nvidia-smi -lms 20"
             self.thread.start()
         except Exception:
             self.proc = None
         return self
 
-    def _pump(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
-            time.sleep(0.15)
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 2 + len(REASONS):
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for r, v in zip(REASONS, parts[2:]):
-                if v.lower() == "active":
-                    reasons.add(r)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": self.source}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 def gpu_id(local: int) -> str:

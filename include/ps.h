@@ -18,9 +18,14 @@
  *     periodic grids hold the n x n independent nodes; the reference's alias row/col n
  *     is the first image row/col.
  *   - Calls are asynchronous on the given stream (NULL = legacy default stream), never
- *     allocate device memory, and are safe from concurrent threads.  The only library
- *     state is a mutex-guarded cache of instantiated CUDA graphs (ps_march) and the
- *     per-launch tile counters of the streaming kernel.
+ *     allocate device memory, and are safe from concurrent threads and streams.  The only
+ *     library state is a mutex-guarded cache of instantiated CUDA graphs (ps_march; the
+ *     lock is held until a cached graph has been launched, so no thread can evict it in
+ *     between) and the tile counters of the streaming kernels: every direct launch takes
+ *     the next of 2048 counter slots (so fewer than 2048 launches of this library may be
+ *     in flight at once), every kernel node of a captured CUDA graph — ps_march's own or a
+ *     caller's stream capture around these calls — owns a slot of a separate pool of 2048
+ *     for the life of the graph (PS_ERR_CUDA once that pool is exhausted).
  *   - Return 0 (PS_OK) or a distinct ps_status; ps_strerror() names it.
  */
 #ifndef PS_H_

@@ -169,6 +169,18 @@ def current_stream():
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def sync_stream(stream):
+    """Block until the work queued on ``stream`` (a ``c_void_p`` handle) has finished."""
+    torch = _torch()
+    handle = getattr(stream, "value", stream) or 0
+    if handle == torch.cuda.current_stream().cuda_stream:
+        torch.cuda.current_stream().synchronize()
+    elif handle == 0:
+        torch.cuda.default_stream().synchronize()
+    else:
+        torch.cuda.ExternalStream(handle).synchronize()
+
+
 def make_table(pairs) -> PsTable:
     """Pack ``[((q1, q2), coeff), ...]`` (dict order) into a ``ps_table``."""
     pairs = list(pairs)
@@ -236,7 +248,7 @@ class Level:
         check(load_library().ps_copy_out(ctypes.byref(self.grid), self.ptr,
                                          out.ctypes.data_as(ctypes.c_void_p), rows, cols, cols,
                                          D2H, st), "ps_copy_out")
-        _torch().cuda.current_stream().synchronize()
+        sync_stream(st)     # the stream the copy ran on, not necessarily the current one
         return out
 
     def fill_ghosts(self, keep_alias=False, stream=None):

@@ -40,7 +40,13 @@ namespace ps {
 
 // launch accounting / per-launch tile-counter slots (defined in ps_device.cu)
 extern std::atomic<int64_t> g_launches;
-extern std::atomic<uint64_t> g_launch_seq;
+// Tile-counter slot of the next launch on `st` (ps_stream.cuh: g_tile_next/g_tile_done):
+// direct launches cycle through [0, kDirectSlots); a launch recorded into a CUDA graph
+// (stream capture) draws a slot from a separate pool that direct launches never touch and
+// keeps it for the life of the graph.  -1: the graph pool is exhausted.
+int launch_slot(cudaStream_t st);
+// Device index clamped to the per-device caches below.
+int device_index();
 
 #include "ps_stream.cuh"
 
@@ -51,16 +57,15 @@ extern std::atomic<uint64_t> g_launch_seq;
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
+constexpr int kMaxDevices = 64;
 struct DevInfo {
   int nsm = 0;
 };
 inline DevInfo dev_info() {
   static std::mutex mu;
-  static DevInfo cache[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
+  static DevInfo cache[kMaxDevices];
+  const int dev = device_index();
   std::lock_guard<std::mutex> lk(mu);
-  if (dev < 0 || dev >= 64) dev = 0;
   if (cache[dev].nsm == 0) cudaDeviceGetAttribute(&cache[dev].nsm, cudaDevAttrMultiProcessorCount, dev);
   return cache[dev];
 }
@@ -210,14 +215,18 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   constexpr int NS = PS_NS;
   using Gm = StreamGeom<T, NW, RB, NS>;
   auto kern = k_two_step_stream<T, A, S, PER, NW, RB, NS, VP>;
-  static std::once_flag once;
-  static int blocks_per_sm = 1;
-  std::call_once(once, [&] {
+  // the shared-memory opt-in is a per-device function attribute: once per device
+  static std::once_flag once[kMaxDevices];
+  static int bps[kMaxDevices];
+  const int dev = device_index();
+  std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, (NW + 1) * 32,
+    bps[dev] = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[dev], kern, (NW + 1) * 32,
                                                   Gm::smem_bytes);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    if (bps[dev] < 1) bps[dev] = 1;
   });
+  const int blocks_per_sm = bps[dev];
   StreamParams p;
   std::memset(&p, 0, sizeof(p));
   p.uk = at_origin<T>(g, uk);
@@ -265,7 +274,8 @@ static ps_status launch_stream(const ps_grid* g, const void* uk, const void* ukm
   const int64_t nchunks = (nrows + rc - 1) / rc;
   p.ntiles = int32_t(nchunks * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
-  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  const int slot = launch_slot(st);
+  if (slot < 0) return PS_ERR_CUDA;
   if (launch_pdl(kern, grid, (NW + 1) * 32, Gm::smem_bytes, st, p, slot) != cudaSuccess)
     return PS_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -368,14 +378,16 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
-  static std::once_flag once;
-  static int blocks_per_sm = 1;
-  std::call_once(once, [&] {
+  static std::once_flag once[kMaxDevices];
+  static int bps[kMaxDevices];
+  const int dev = device_index();
+  std::call_once(once[dev], [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Gm::smem_bytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, NT,
-                                                  Gm::smem_bytes);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    bps[dev] = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[dev], kern, NT, Gm::smem_bytes);
+    if (bps[dev] < 1) bps[dev] = 1;
   });
+  const int blocks_per_sm = bps[dev];
   const int64_t nrows = rhi - rlo;
   if (nrows <= 0) return PS_OK;
   TBParams p;
@@ -427,7 +439,8 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.rc = rc;
   p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
   const int grid = int(std::min<int64_t>(p.ntiles, resident));
-  const int slot = int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kSlots);
+  const int slot = launch_slot(st);
+  if (slot < 0) return PS_ERR_CUDA;
   if (launch_pdl(kern, grid, NT, Gm::smem_bytes, st, p, slot) != cudaSuccess)
     return PS_ERR_CUDA;
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -12,7 +12,48 @@
 namespace ps {
 
 std::atomic<int64_t> g_launches{0};
-std::atomic<uint64_t> g_launch_seq{0};
+
+int device_index() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) cudaGetLastError();
+  return (dev < 0 || dev >= kMaxDevices) ? 0 : dev;
+}
+
+// Tile-counter slots (ps_stream.cuh).  Direct launches: a sequence number modulo
+// kDirectSlots.  Launches recorded by stream capture: a slot of the graph pool, returned
+// to the pool when the cached graph that owns it is evicted (cycle_graph records them
+// through t_capture_slots); a caller's own capture keeps its slots for the process life.
+static std::atomic<uint64_t> g_launch_seq{0};
+static std::mutex g_slot_mu;
+static std::vector<int> g_graph_free;
+static int g_graph_hi = kDirectSlots;
+static thread_local std::vector<int>* t_capture_slots = nullptr;
+
+int launch_slot(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    cs = cudaStreamCaptureStatusNone;
+  }
+  if (cs != cudaStreamCaptureStatusActive)
+    return int(g_launch_seq.fetch_add(1, std::memory_order_relaxed) % kDirectSlots);
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  int slot = -1;
+  if (!g_graph_free.empty()) {
+    slot = g_graph_free.back();
+    g_graph_free.pop_back();
+  } else if (g_graph_hi < kSlots) {
+    slot = g_graph_hi++;
+  }
+  if (slot >= 0 && t_capture_slots) t_capture_slots->push_back(slot);
+  return slot;
+}
+
+static void release_slots(std::vector<int>& slots) {
+  std::lock_guard<std::mutex> lk(g_slot_mu);
+  g_graph_free.insert(g_graph_free.end(), slots.begin(), slots.end());
+  slots.clear();
+}
 
 #include "ps_errsum.cuh"
 #include "ps_batch.cuh"
@@ -117,6 +158,7 @@ struct GraphKey {
 struct GraphEntry {
   GraphKey key;
   cudaGraphExec_t exec;
+  std::vector<int> slots;  // tile-counter slots its kernel nodes own
 };
 static std::mutex g_graph_mu;
 static GraphEntry g_graphs[32];
@@ -130,6 +172,8 @@ static cudaStream_t capture_stream(int dev) {
   return streams[dev];
 }
 
+// Caller holds g_graph_mu and keeps it until the returned exec has been launched (another
+// thread could otherwise evict and destroy it between lookup and cudaGraphLaunch).
 static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, const ps_table* t) {
   GraphKey key;
   std::memset(&key, 0, sizeof(key));
@@ -143,7 +187,6 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
     key.t.q2[s] = t->q2[s];
     key.t.c[s] = t->c[s];
   }
-  std::lock_guard<std::mutex> lk(g_graph_mu);
   for (int e = 0; e < g_ngraphs; ++e)
     if (std::memcmp(&g_graphs[e].key, &key, sizeof(key)) == 0) return g_graphs[e].exec;
   cudaStream_t cs = capture_stream(key.dev);
@@ -152,6 +195,8 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
     cudaGetLastError();
     return nullptr;
   }
+  std::vector<int> slots;
+  t_capture_slots = &slots;
   int c = cur;
   ps_status st = PS_OK;
   for (int k = 0; k < kGraphCycle && st == PS_OK; ++k) {
@@ -159,6 +204,7 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
                        march_opts(g, k));
     c = (c + 1) % 3;
   }
+  t_capture_slots = nullptr;
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
   cudaGraphExec_t exec = nullptr;
@@ -166,14 +212,23 @@ static cudaGraphExec_t cycle_graph(const ps_grid* g, void* lvl[3], int cur, cons
       cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
+    release_slots(slots);
     return nullptr;
   }
   cudaGraphDestroy(graph);
   g_launches.fetch_sub(kGraphCycle, std::memory_order_relaxed);  // captured, not executed
   GraphEntry& slot = g_graphs[g_graph_next];
-  if (g_graph_next < g_ngraphs && slot.exec) cudaGraphExecDestroy(slot.exec);
+  if (g_graph_next < g_ngraphs && slot.exec) {
+    // an evicted graph may still be executing: its slots go back only once it is destroyed
+    // (cudaGraphExecDestroy defers the release until the running launch completes, but the
+    // counters must not be handed to a new graph before then)
+    cudaDeviceSynchronize();
+    cudaGraphExecDestroy(slot.exec);
+    release_slots(slot.slots);
+  }
   slot.key = key;
   slot.exec = exec;
+  slot.slots = std::move(slots);
   g_graph_next = (g_graph_next + 1) % 32;
   g_ngraphs = std::min(g_ngraphs + 1, 32);
   return exec;
@@ -420,6 +475,7 @@ ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_tabl
   int cur = *newest;
   int64_t k = 0;
   if (nsteps >= 2 * kGraphCycle && env_int("PS_GRAPH", 1) != 0) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);  // held across the launches (see cycle_graph)
     if (cudaGraphExec_t exec = cycle_graph(g, lvl, cur, t)) {
       for (; k + kGraphCycle <= nsteps; k += kGraphCycle) {
         if (cudaGraphLaunch(exec, st) != cudaSuccess) return PS_ERR_CUDA;
@@ -794,8 +850,8 @@ ps_status ps_batch_run(int32_t nsim, int32_t max_n, const void* desc_dev, const 
   const size_t nn = size_t(max_n + 1) * size_t(max_n + 1);
   const size_t smem = 3 * nn * sizeof(double) + 4 * ps::kBatchMaxLeaves * sizeof(double) +
                       (4 * ps::kBatchMaxLeaves + 2) * sizeof(int);
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::once_flag once[ps::kMaxDevices];  // per-device function attribute
+  std::call_once(once[ps::device_index()], [] {
     cudaFuncSetAttribute(ps::k_batch_run, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
   });

@@ -104,10 +104,15 @@ struct StreamGeom {
       size_t(NS) * RB * (SU + W) * sizeof(T) + 2 * NS * sizeof(uint64_t) + 2 * NS * sizeof(int);
 };
 
-// Dynamic tile scheduler: one counter pair per in-flight launch (slot = launch
-// sequence number mod kSlots).  The last block to finish resets its slot, so the next
-// launch that reuses it (kSlots launches later) starts from zero.
-constexpr int kSlots = 1024;
+// Dynamic tile scheduler: one counter pair per in-flight launch.  The last block to
+// finish resets its slot, so the next launch that reuses it starts from zero.  Slots are
+// handed out by launch_slot() (ps_device.cu): direct launches cycle through
+// [0, kDirectSlots) — safe while fewer than kDirectSlots launches of this library are in
+// flight at once — and every kernel node of a captured CUDA graph owns a slot of
+// [kDirectSlots, kSlots) that no direct launch or other graph uses (a graph's replays are
+// serialised by CUDA, so its nodes never race with themselves).
+constexpr int kSlots = 4096;
+constexpr int kDirectSlots = 2048;
 static __device__ unsigned int g_tile_next[kSlots];
 static __device__ unsigned int g_tile_done[kSlots];
 

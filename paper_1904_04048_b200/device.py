@@ -193,6 +193,10 @@ class Simulation:
         if getattr(self, "_stage", None) is None:
             self._stage = nat.Level(self.grid)
             self._side = torch.cuda.Stream()
+            self._stage_free = None
+        if self._stage_free is not None:
+            # the staging level is still the source of the previous snapshot's D2H copy
+            torch.cuda.current_stream().wait_event(self._stage_free)
         self._stage.buf.copy_(self.levels[idx].buf)
         ready = torch.cuda.Event()
         ready.record()
@@ -207,6 +211,7 @@ class Simulation:
                 nat.D2H, ctypes.c_void_p(self._side.cuda_stream)), "ps_copy_out")
             done = torch.cuda.Event()
             done.record(self._side)
+        self._stage_free = done
 
         def write():
             done.synchronize()
@@ -218,6 +223,9 @@ class Simulation:
 
     def save_checkpoint(self, path):
         """Persist what a restart needs: both live levels (u^k, u^{k-1}) and k."""
+        if self.newest is None or self.previous is None:
+            raise RuntimeError("nothing to checkpoint: call first_step() first (a restart "
+                               "needs two live levels)")
         np.savez(path, newest=self.field("newest"), previous=self.field("previous"),
                  step=self.step, n=self.n, lam=self.lam, bc=self.bc, dtype=self.dtype,
                  scheme=self.spec.name)
@@ -227,6 +235,10 @@ class Simulation:
         ck = np.load(path)
         if int(ck["n"]) != self.n or str(ck["bc"]) != self.bc or str(ck["dtype"]) != self.dtype:
             raise ValueError("checkpoint does not match this simulation's grid")
+        if str(ck["scheme"]) != self.spec.name or float(ck["lam"]) != self.lam:
+            raise ValueError(f"checkpoint was written by scheme {ck['scheme']} at lambda "
+                             f"{float(ck['lam'])!r}, this simulation runs {self.spec.name} at "
+                             f"{self.lam!r}")
         self.levels[2].upload(ck["newest"])
         self.levels[1].upload(ck["previous"])
         if self.bc == "periodic":

@@ -149,6 +149,30 @@ def test_oracle_matches_reference_golden_marches(runs, fields, oracle):
         assert last.tobytes() == fields[m["key"] + "_last"].tobytes(), m["key"]
 
 
+def test_numpy_restatement_matches_reference_golden_calls(runs, fields, oracle):
+    """oracle/numpy_ref.py (the reference's array algorithm, bench.py's 1-core CPU leg) is
+    bitwise equal to every golden call, and its slab form to the C oracle's row range."""
+    from oracle import numpy_ref as N
+
+    for case in runs["cases"]:
+        spec = ps.named_scheme(case["scheme"])
+        key, bc, lam = case["key"], case["bc"], case["lam"]
+        a, b = fields[key + "_a"], fields[key + "_b"]
+        two = N.two_step(a, b, _pairs(spec, "two_step", lam), bc, 1)
+        first = N.first_step(a, b, _pairs(spec, "first_u", lam), _pairs(spec, "first_v", lam),
+                             case["tau"], bc, 1)
+        assert two.dtype == fields[key + "_two"].dtype
+        assert two.tobytes() == fields[key + "_two"].tobytes(), key
+        assert first.tobytes() == fields[key + "_first"].tobytes(), key
+    rng = np.random.default_rng(5)
+    for name, ring, dt in (("P9", 1, np.float64), ("P13", 2, np.float64), ("P13", 2, np.float32)):
+        pairs = _pairs(ps.named_scheme(name), "two_step", 0.4)
+        a = rng.standard_normal((37, 53)).astype(dt)
+        b = rng.standard_normal((37, 53)).astype(dt)
+        assert N.two_step_slab(a, b, pairs, ring).tobytes() == \
+            oracle.two_step(a, b, pairs, "dirichlet", ring).tobytes()
+
+
 def test_oracle_ring_generalisation_reduces_to_reference(fields, runs, oracle):
     """Ring width r=2 for radius-1 tables: ring of zeros two wide, interior unchanged
     except rows/cols 1 and n-1 (now pinned) — i.e. exactly the r=1 result restricted."""
