@@ -255,6 +255,88 @@ def cpu_sample(cfg, seconds: float, threads: int = 0, rows_hint: int | None = No
     return rate, rows, 4, dt
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def numpy_sample(cfg, seconds: float):
+    """Time oracle/numpy_ref.py — the reference's own array algorithm (one temporary and
+    one add pass per tap, np.roll per tap when periodic; simulator.py:147-191), which is
+    single-threaded — on a bounded full-width slab.  Returns (LUP/s, rows, steps, secs)."""
+    import numpy as np
+
+    from oracle import numpy_ref as N
+    from paper_1904_04048_b200.scheme import evaluate_table, named_scheme
+
+    pairs = evaluate_table(named_scheme(cfg["scheme"]).two_step, cfg["lam"])
+    npdt = np.float64 if cfg["dtype"] == "f64" else np.float32
+    width = cfg["n"] + 1
+    rng = np.random.default_rng(0)
+    if cfg["bc"] == "periodic":
+        # np.roll wraps both axes, so the periodic call is timed on a square grid of the
+        # same algorithm: the whole config when small, else the largest square within budget
+        def run(n, steps):
+            a = rng.standard_normal((n + 1, n + 1)).astype(npdt)
+            b = rng.standard_normal(a.shape).astype(npdt)
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                a, b = N.two_step(a, b, pairs, "periodic"), a
+            return n * n * steps / (time.perf_counter() - t0), time.perf_counter() - t0
+
+        n = min(cfg["n"], 1024)
+        rate, dt = run(n, 1)
+        n = int(min(cfg["n"], max(256, (seconds / 3.0 * rate) ** 0.5)))
+        rate, dt = run(n, 3)
+        return rate, n, 3, dt, f"{n}^2 periodic grid"
+    ring = max(cfg["ring"], 1)
+
+    def run(rows, steps):
+        a = rng.standard_normal((rows + 2 * ring, width)).astype(npdt)
+        b = rng.standard_normal(a.shape).astype(npdt)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            a, b = N.two_step_slab(a, b, pairs, ring), a
+        dt = time.perf_counter() - t0
+        return rows * (width - 2 * ring) * steps / dt, dt
+
+    rows = max(8, min(width - 2 * ring, 4_000_000 // width))
+    rate, dt = run(rows, 1)
+    rows = int(max(8, min(width - 2 * ring, seconds / 3.0 * rate / width)))
+    rate, dt = run(rows, 3)
+    return rate, rows, 3, dt, f"{rows} full-width rows x {width} cols"
+
+
+def cpu_baseline(args, cfg):
+    """The reference's CPU path on this box's host cores, beside the GPU number: the C
+    port on all cores (`value`) and the reference's numpy algorithm on its one core."""
+    from oracle import oracle as O
+
+    rate, rows, steps, secs = cpu_sample(cfg, args.cpu_seconds)
+    out = {"value": rate / 1e9, "unit": "GLUP/s", "cores": O.max_threads(), "kind": "port",
+           "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+           "sample": f"{rows} full-width rows x {cfg['n'] + 1} cols, {steps} two-step updates "
+                     f"({secs:.1f} s) through oracle/ps_oracle.c (reference arithmetic, OpenMP)"}
+    try:
+        nrate, _, nsteps, nsecs, what = numpy_sample(cfg, min(args.cpu_seconds, 8.0))
+        out["numpy_reference_algorithm"] = {
+            "value": nrate / 1e9, "unit": "GLUP/s", "cores": 1,
+            "cores_note": f"1 core of {os.cpu_count()} (numpy ufuncs are single-threaded)",
+            "kind": "port",
+            "sample": f"{what}, {nsteps} two-step updates ({nsecs:.1f} s) through "
+                      "oracle/numpy_ref.py (the reference's per-tap slice/roll passes, "
+                      "simulator.py:147-191; the package itself cannot travel to this box)"}
+    except MemoryError:
+        out["numpy_reference_algorithm"] = None
+    return out
+
+
 def reference_arm(args, cfg, cfg_name):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -295,8 +377,11 @@ def reference_arm(args, cfg, cfg_name):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-        "config": {"workload": cfg["desc"], "parallelism": "cpu"},
+        "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
+                   "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
+                   "parallelism": "cpu (OpenMP over rows)"},
         "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
                          "sample": sample + "; oracle/ps_oracle.c (reference arithmetic, "
                                    "OpenMP over rows)"},
         "e2e": {"value": value, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -330,7 +415,9 @@ def make_sim(cfg, tsteps=1):
 
 def measure_march(args, cfg, T):
     """Build the config's grid, first step, warm up, then time K march steps at temporal
-    blocking depth T with CUDA events on the launching stream."""
+    blocking depth T with CUDA events on the launching stream.  The K-step region is
+    repeated (``--reps``; auto: 3 while one region takes under 2 s) and the MEDIAN region is
+    reported, with the clock sampler running across all repetitions."""
     import torch
 
     from paper_1904_04048_b200 import _native as nat
@@ -338,56 +425,109 @@ def measure_march(args, cfg, T):
     sim = make_sim(cfg, T)
     sim.first_step()
     stream = torch.cuda.current_stream()
-    # warm-up also instantiates ps_march's CUDA graph (captured for runs of >= 12 steps)
-    warm = max(args.warmup, 12)
-    sim.march(warm)
-    torch.cuda.synchronize()
     K = args.steps
-    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = nat.launch_count()
+    warm = args.warmup
+    if warm:
+        sim.march(warm)
+    extra = None
+    if T == 1 and K >= 12:
+        # ps_march replays a CUDA graph for calls of >= 12 steps; instantiate it outside
+        # the timed region with one extra 12-step call (reported, not hidden in `warmup`)
+        sim.march(12)
+        extra = {"steps": 12, "why": "one untimed 12-step ps_march call instantiates the "
+                                      "CUDA graph the timed call replays"}
+    torch.cuda.synchronize()
+    regions, launches = [], 0
+    reps = args.reps if args.reps > 0 else 3
     with ClockSampler(gpu_id(0)) as clk:
-        torch.cuda.synchronize()
-        t_begin.record(stream)
-        sim.march(K)          # K updates: back-to-back hot-kernel launches on one stream
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    launches = nat.launch_count() - launches0
-    total_ms = t_begin.elapsed_time(t_end)
+        for rep in range(reps):
+            t_begin, t_end = (torch.cuda.Event(enable_timing=True),
+                              torch.cuda.Event(enable_timing=True))
+            launches0 = nat.launch_count()
+            torch.cuda.synchronize()
+            t_begin.record(stream)
+            sim.march(K)      # K updates: back-to-back hot-kernel launches on one stream
+            t_end.record(stream)
+            torch.cuda.synchronize()
+            launches = nat.launch_count() - launches0
+            regions.append(t_begin.elapsed_time(t_end))
+            if args.reps <= 0 and regions[0] > 2000.0:
+                break
+    total_ms = statistics.median(regions)
     lup_step = sim.updated_nodes
-    # algorithmic HBM words per update: 3 (read u^k, u^{k-1}; write u^{k+1}); at temporal
-    # blocking depth T one launch reads 2 levels and writes 2 for T updates
-    words_per_lup = 3.0 if T == 1 else 4.0 / T
-    bytes_launch = words_per_lup * T * sim.itemsize * lup_step
     avg_launch_ms = total_ms / K * T      # K/T launches of T fused updates each
     peak, peak_src = load_peak()
+    # algorithmic traffic = 3 words per update (read u^k, u^{k-1}, write
+    # u^{k+1}); a launch of depth T performs T * lup_step updates
+    bytes_launch = 3.0 * T * sim.itemsize * lup_step
     achieved = bytes_launch / (avg_launch_ms * 1e-3) / 1e9
-    return {"sim": sim, "T": T, "K": K, "warmup": warm, "total_ms": total_ms,
+    # what the launch must move through DRAM: a fused pass of depth T reads two levels
+    # and writes two for T updates (4/T words per update); T = 1 moves the 3 words
+    dram_words = 3.0 if T == 1 else 4.0 / T
+    dram_model = dram_words * T * sim.itemsize * lup_step
+    return {"sim": sim, "T": T, "K": K, "warmup": warm, "warmup_extra": extra,
+            "total_ms": total_ms, "regions_ms": regions,
             "value": lup_step * K / (total_ms * 1e-3) / 1e9, "launches": launches,
-            "clocks": clk.summary(), "lup_step": lup_step, "words_per_lup": words_per_lup,
-            "bytes_launch": bytes_launch, "avg_launch_ms": avg_launch_ms, "peak": peak,
-            "peak_src": peak_src, "achieved": achieved}
+            "clocks": clk.summary(), "lup_step": lup_step, "bytes_launch": bytes_launch,
+            "avg_launch_ms": avg_launch_ms, "peak": peak, "peak_src": peak_src,
+            "achieved": achieved, "dram_words": dram_words, "dram_model": dram_model,
+            "dram_achieved": dram_model / (avg_launch_ms * 1e-3) / 1e9}
+
+
+def roofline_block(m, cfg_name):
+    """The `roofline` object (prompt ④ / SURVEY.md §8d D2) plus the DRAM-side view."""
+    T = m["T"]
+    traffic = load_traffic(cfg_name, T)
+    roof = {"bound": "hbm", "achieved": m["achieved"], "peak": m["peak"], "unit": "GB/s",
+            "frac": m["achieved"] / m["peak"], "traffic": traffic,
+            "peak_source": m["peak_src"],
+            "algorithmic_bytes_per_launch": m["bytes_launch"],
+            "bytes_per_lup": 3 * m["sim"].itemsize,
+            "lup_per_launch": m["lup_step"] * T,
+            "kernel_ms_per_launch": m["avg_launch_ms"],
+            "definition": "SURVEY.md §8(d): 3 words per update x updates per launch / mean "
+                          "launch duration (CUDA events over the timed region), over the "
+                          "measured HBM copy peak"}
+    if T > 1:
+        roof["note"] = (f"temporal blocking T={T} fuses {T} updates per pass, so a launch does "
+                        f"{T}x the single-update algorithmic bytes while moving 4/T words per "
+                        "update through DRAM: frac > 1 is expected (SURVEY.md §8d); `dram` "
+                        "below is the memory-side fraction, `compute_roofline` the binding one")
+    dram = {"model_words_per_lup": m["dram_words"], "model_bytes_per_launch": m["dram_model"],
+            "achieved_gbs": m["dram_achieved"], "frac_of_peak": m["dram_achieved"] / m["peak"],
+            "ncu_bytes_per_launch": traffic,
+            "ncu_over_model": (traffic / m["dram_model"]) if traffic else None,
+            "note": "bytes a launch must move through DRAM (T=1: 3 words/update; depth T: 2 "
+                    "levels read + 2 written per T updates) / launch duration; ncu figure = "
+                    "dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                    "(profiles/ncu_<config>[_T<depth>].json)"}
+    return roof, dram
 
 
 def gpu_arm_single(args, cfg, cfg_name):
     import torch
 
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device visible (there is no CPU fallback; "
+                         "`--impl reference` times the CPU path)")
     torch.cuda.set_device(torch.device("cuda", 0))
-    tb_ok = True
     # auto: the fastest measured depth per config (DESIGN.md §9), 1 where blocking is n/a
-    T = args.tsteps if args.tsteps > 0 else (cfg.get("tb", 1) if tb_ok else 1)
+    T = args.tsteps if args.tsteps > 0 else cfg.get("tb", 1)
     companion = None
     if T > 1 and args.tsteps == 0:
         # also time the unblocked march (one update per launch) for the roofline story
         c1 = measure_march(args, cfg, 1)
+        r1, d1 = roofline_block(c1, cfg_name)
         companion = {"temporal_blocking": 1, "value": c1["value"], "unit": "GLUP/s",
                      "ms_per_step": c1["total_ms"] / c1["K"],
-                     "roofline_frac": c1["achieved"] / c1["peak"],
-                     "achieved_gbs": c1["achieved"], "clocks": c1["clocks"]}
+                     "roofline_frac": r1["frac"], "achieved_gbs": c1["achieved"],
+                     "traffic": r1["traffic"], "regions_ms": c1["regions_ms"],
+                     "warmup_extra": c1["warmup_extra"], "clocks": c1["clocks"]}
         del c1
         torch.cuda.empty_cache()
     m = measure_march(args, cfg, T)
     sim = m["sim"]
-    lup_roofline = m["peak"] / (3 * sim.itemsize)   # HBM-roofline LUP/s of one update
+    roof, dram = roofline_block(m, cfg_name)
     line = {
         "metric": METRIC, "value": m["value"], "unit": "GLUP/s", "n_gpus": 1, "steps": m["K"],
         "warmup": m["warmup"], "ms_per_step": m["total_ms"] / m["K"], "higher_is_better": True,
@@ -399,39 +539,33 @@ def gpu_arm_single(args, cfg, cfg_name):
                    "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
                          "streamed from HBM every launch" if sim.level_bytes > 126e6 else
                          "grid fits in L2 (latency-bound correctness config)"},
-        "roofline": {"bound": "hbm", "achieved": m["achieved"], "peak": m["peak"], "unit": "GB/s",
-                     "frac": m["achieved"] / m["peak"], "traffic": load_traffic(cfg_name, T),
-                     "peak_source": m["peak_src"],
-                     "algorithmic_bytes_per_launch": m["bytes_launch"],
-                     "kernel_ms_per_launch": m["avg_launch_ms"],
-                     "lup_per_launch": m["lup_step"] * T,
-                     "bytes_per_lup": m["words_per_lup"] * sim.itemsize,
-                     **({"note": f"temporal blocking T={T}: the fused kernel moves 4/T words "
-                                 "per update, so it runs below the HBM bound — it is FP64/"
-                                 "FP32 issue-bound (ncu pipe utilisation in profiles/); "
-                                 "lup_roofline compares against the single-update roofline"}
-                        if T > 1 else {})},
-        # BASELINE's "fraction of HBM roofline" in update terms: value / (HBM GB/s / 3 words)
-        "lup_roofline": {"glups": lup_roofline, "frac": m["value"] / lup_roofline,
-                         "note": "single-update roofline (3 words/LUP); temporal blocking "
-                                 "moves 4/T words/LUP, so it can exceed 1"},
+        "timing": {"regions_ms": m["regions_ms"], "reported": "median region",
+                   "what": f"{len(m['regions_ms'])} back-to-back regions of exactly "
+                           f"{m['K']} steps, each between CUDA events on the launching stream"},
+        "roofline": roof,
+        "dram": dram,
         "clocks": m["clocks"],
         "gpu_launches": m["launches"],
     }
+    if m["warmup_extra"]:
+        line["warmup_extra"] = m["warmup_extra"]
+    if cfg["dtype"] == "f32":
+        line["config"]["arith_note"] = (
+            "native = the GPU's own f32 contract (one fma per tap, f32 accumulator), narrower "
+            "than the reference's float32 path (f32 products summed in f64); the reference "
+            "contract (--arith ref, bitwise = numpy) is conversion-bound, see DESIGN.md §9"
+            if cfg["arith"] == "native" else
+            "ref = the reference's float32 sequence (f32 products, f64 accumulator), bitwise")
     if T > 1:
         line["compute_roofline"] = compute_roofline(cfg, m["value"])
     if companion:
         line["unblocked_companion"] = companion
     if not args.no_e2e:
         line["e2e"] = e2e_single(args, cfg, sim)
+    del m, sim
+    torch.cuda.empty_cache()
     if not args.no_cpu:
-        from oracle import oracle as O
-
-        rate, rows, steps, secs = cpu_sample(cfg, args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": rate / 1e9, "unit": "GLUP/s", "cores": O.max_threads(), "kind": "port",
-            "sample": f"{rows} full-width rows x {cfg['n'] + 1} cols, {steps} two-step updates "
-                      f"({secs:.1f} s) through oracle/ps_oracle.c (reference arithmetic, OpenMP)"}
+        line["cpu_baseline"] = cpu_baseline(args, cfg)
     print(json.dumps(line), flush=True)
 
 
@@ -462,6 +596,9 @@ def e2e_single(args, cfg, sim):
     K = args.steps
     h2d = pin_u.numel() * pin_u.element_size() * (1 if pin_v is None else 2)
     d2h = out.numel() * out.element_size()
+
+    while len(sim.levels) < 4:          # ps_solve_host wants four scratch levels
+        sim.levels.append(nat.Level(sim.grid))
 
     def solve():
         nat.solve_host(g, sim.levels[:4], pin_u.data_ptr(),
@@ -503,7 +640,11 @@ def e2e_single(args, cfg, sim):
     ms, launches, clocks = timed(solve)
     return {"value": sim.updated_nodes * K / (ms * 1e-3) / 1e9, "unit": "GLUP/s",
             "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-            "ms_total": ms, "gpu_launches": launches, "clocks": clocks,
+            "steps": K, "ms_total": ms, "gpu_launches": launches, "clocks": clocks,
+            "pcie_gbs": (h2d + d2h) / (ms * 1e-3) / 1e9,
+            "note": f"one solve of {K} steps: {h2d / 1e9:.2f} GB in + {d2h / 1e9:.2f} GB out cross "
+                    "PCIe once per solve, so short solves are copy-bound and the figure grows "
+                    "with the step count (BASELINE step counts: --steps unset)",
             "what": "ps_solve_host: pinned host u0[,v0] in, u^K out to pinned host; row bands "
                     "marched as a skewed wavefront so the PCIe copies overlap the march "
                     "(one CUDA-event-timed region on the caller's stream)",
@@ -513,7 +654,10 @@ def e2e_single(args, cfg, sim):
                                    "no overlap"}}
 
 
-def gpu_arm_dist(args, cfg, cfg_name):
+def dist_measure(args, cfg, T, keep_ics):
+    """One row-slab march on this rank's slab at temporal-blocking depth T: seeded ICs on
+    the device, halo exchange, first step, warm-up, then K steps between barriers and CUDA
+    events; the reported time is the max over ranks."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -522,18 +666,11 @@ def gpu_arm_dist(args, cfg, cfg_name):
     from paper_1904_04048_b200.device import gaussian_params
     from paper_1904_04048_b200.slab import DistributedSlabs
 
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if cfg["bc"] != "dirichlet" or not isinstance(cfg["ic"], tuple):
-        raise SystemExit("multi-GPU bench supports the Dirichlet Gaussian configs (C3-C5)")
+    _, _, local = dist_env()
     K = args.steps
-    T = args.tsteps if args.tsteps > 0 else cfg.get("tb", 1)
-    while T > 1 and K % T:      # the timed region must hold whole blocked passes
-        T //= 2
     slab = DistributedSlabs(cfg["scheme"], cfg["n"], cfg["lam"], ring=cfg["ring"],
                             dtype=cfg["dtype"], arith=cfg["arith"], transport=args.transport,
-                            tsteps=T)
+                            tsteps=T, graph=not args.no_graph)
     K0, wmin, wmax, vzero = cfg["ic"]
     rng = np.random.default_rng(0)
     pu = gaussian_params(rng, K0, wmin, wmax)
@@ -546,12 +683,13 @@ def gpu_arm_dist(args, cfg, cfg_name):
     slab.exchange(1)
     slab.exchange(0)
     ics = None
-    if not args.no_e2e:  # keep this rank's rows of u0 / v0 for the end-to-end leg
+    if keep_ics:  # keep this rank's rows of u0 / v0 for the end-to-end leg
         ics = (torch.from_numpy(slab.levels[1].download()).pin_memory(),
                None if vzero else torch.from_numpy(slab.levels[0].download()).pin_memory())
     slab.first_step()
-    warm = max(T, (args.warmup + T - 1) // T * T)
-    slab.march(warm)
+    warm = (args.warmup + T - 1) // T * T      # whole passes (rounded up, reported)
+    if warm:
+        slab.march(warm)
     torch.cuda.synchronize()
     dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -568,36 +706,83 @@ def gpu_arm_dist(args, cfg, cfg_name):
     ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
-    e2e = None if args.no_e2e else e2e_dist(args, cfg, slab, dist, ics)
     inner = cfg["n"] + 1 - 2 * cfg["ring"]
-    lup_step = inner * inner
-    value = lup_step * K / (total_ms * 1e-3) / 1e9
+    return {"slab": slab, "ics": ics, "T": T, "K": K, "warmup": warm, "total_ms": total_ms,
+            "value": inner * inner * K / (total_ms * 1e-3) / 1e9, "launches": launches,
+            "clocks": clk.summary(), "lup_step": inner * inner, "graphed": slab.graphed}
+
+
+def gpu_arm_dist(args, cfg, cfg_name):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs CUDA device {local}; "
+                         f"{torch.cuda.device_count()} visible (no CPU fallback)")
+    # the driver's rank check reads NCCL's own init lines
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if cfg["bc"] != "dirichlet" or not isinstance(cfg["ic"], tuple):
+        raise SystemExit("multi-GPU bench supports the Dirichlet Gaussian configs (C3-C5)")
+    K = args.steps
+    T = args.tsteps if args.tsteps > 0 else cfg.get("tb", 1)
+    while T > 1 and K % T:      # the timed region must hold whole blocked passes
+        T -= 1
+    companion = None
+    if T > 1 and args.tsteps == 0:
+        # the literal config ("per-step halo exchange of R rows per neighbour"): T = 1
+        c1 = dist_measure(args, cfg, 1, False)
+        companion = {"temporal_blocking": 1, "value": c1["value"], "unit": "GLUP/s",
+                     "ms_per_step": c1["total_ms"] / K, "gpu_launches": c1["launches"],
+                     "halo": f"{c1['slab'].R} row(s) per neighbour per step",
+                     "cuda_graph": c1["graphed"], "clocks": c1["clocks"]}
+        c1["slab"].close()
+        del c1
+        torch.cuda.empty_cache()
+    m = dist_measure(args, cfg, T, not args.no_e2e)
+    slab, total_ms = m["slab"], m["total_ms"]
+    e2e = None if args.no_e2e else e2e_dist(args, cfg, slab, dist, m["ics"])
+    lup_step = m["lup_step"]
     itemsize = 8 if cfg["dtype"] == "f64" else 4
     peak, peak_src = load_peak()
-    words = 3.0 if T == 1 else 4.0 / T
-    achieved = words * itemsize * lup_step / world / (total_ms / K * 1e-3) / 1e9
+    # per GPU: 3 words per update x this GPU's share of the updates / step time (incl. exchange)
+    achieved = 3.0 * itemsize * lup_step / world / (total_ms / K * 1e-3) / 1e9
+    dram_words = 3.0 if T == 1 else 4.0 / T
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "GLUP/s", "n_gpus": world, "steps": K,
-            "warmup": warm, "ms_per_step": total_ms / K, "higher_is_better": True,
+            "metric": METRIC, "value": m["value"], "unit": "GLUP/s", "n_gpus": world, "steps": K,
+            "warmup": m["warmup"], "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
             "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
-                       "lambda": cfg["lam"], "arith": cfg["arith"], "temporal_blocking": T,
+                       "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
+                       "temporal_blocking": T,
                        "parallelism": f"row slabs x{world}, {slab.R * T}-row halo "
                                       + ("over NCCL send/recv" if args.transport == "nccl" else
                                          "stored into peer ghost rows by the fused kernel "
                                          "(CUDA IPC over NVLink)")
                                       + ", overlapped with the interior update",
+                       "cuda_graph": m["graphed"],
                        "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(cfg_name, T),
-                         "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)"},
-            "clocks": clk.summary(),
-            "gpu_launches": launches,
+                         "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)",
+                         "definition": "SURVEY.md §8(d): 3 words per update x this GPU's "
+                                       "updates per step / step time, over the measured peak"},
+            "dram": {"model_words_per_lup": dram_words,
+                     "achieved_gbs": achieved * dram_words / 3.0,
+                     "frac_of_peak": achieved * dram_words / 3.0 / peak},
+            "clocks": m["clocks"],
+            "gpu_launches": m["launches"],
             "e2e": e2e,
         }
+        if companion:
+            line["unblocked_companion"] = companion
         print(json.dumps(line), flush=True)
+    slab.close()
     dist.destroy_process_group()
 
 
@@ -651,6 +836,27 @@ def e2e_dist(args, cfg, slab, dist, ics):
                     "(bytes per rank)"}
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: check that N GPUs are visible, then
+    re-execute this command line under torch.distributed.run with one rank per GPU."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} visible CUDA devices, found {have}; refusing to "
+              "report a smaller run as an N-GPU number", file=sys.stderr)
+        return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -668,10 +874,16 @@ def main():
                          "sequence with a float64 accumulator; native: one fma per tap)")
     ap.add_argument("--transport", choices=("nccl", "p2p"), default="nccl",
                     help="multi-GPU halo transport")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="multi-GPU: launch each pass eagerly instead of replaying one "
+                         "captured CUDA graph per pass")
     ap.add_argument("--force-dist", action="store_true",
                     help="run the torch.distributed row-slab path even at world size 1 "
                          "(exercises the multi-GPU code on one GPU)")
-    ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 4),
+    ap.add_argument("--reps", type=int, default=0,
+                    help="repetitions of the K-step timed region (median reported); 0 = auto: "
+                         "3 while a region takes under 2 s, else 1")
+    ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 3, 4),
                     help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
                          "C3 f32: 4, C3 f64: 2, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
@@ -685,6 +897,8 @@ def main():
     if args.impl == "reference":
         reference_arm(args, cfg, args.config)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if world > 1 or args.force_dist:
         gpu_arm_dist(args, cfg, args.config)
     else:

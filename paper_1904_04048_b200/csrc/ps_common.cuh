@@ -408,6 +408,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.gmax = int32_t(g->rows + g->ghost);
   p.cmax = int32_t(g->pitch - (g->origin - g->ghost * g->pitch));
   p.reverse = reverse ? 1 : 0;
+  p.row_images = (PER && single_slab(g)) ? 1 : 0;
   p.hu_prev = h.up_prev ? at_origin<T>(g, h.up_prev) : nullptr;
   p.hu_last = h.up_last ? at_origin<T>(g, h.up_last) : nullptr;
   p.hd_prev = h.dn_prev ? at_origin<T>(g, h.dn_prev) : nullptr;
@@ -529,6 +530,7 @@ PS_TYPED_DECL(f32n)
                      bool rev, int rc, const TBHalo& h) {                                   \
     switch (tsteps) {                                                                       \
       case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
+      case 3: return dispatch_tb<T, A, 3>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
       case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
       default: return PS_ERR_ARG;                                                           \
     }                                                                                       \

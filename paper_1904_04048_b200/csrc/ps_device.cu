@@ -135,10 +135,10 @@ static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
                      shape_matches<ShapeC9>(t) || shape_matches<ShapeP13>(t);
   if (!shape || g->rows < 4 || g->cols < 4) return false;
   if (g->bc == PS_BC_DIRICHLET) return true;
-  // periodic: single slab, images to depth R*tsteps must fit the ghost band, and one
-  // wrap must cover them
+  // periodic: images to depth R*tsteps must fit the ghost band, and one wrap (or, for a
+  // row slab of a ring, one neighbour's rows) must cover them
   const int64_t D = int64_t(table_radius(t)) * tsteps;
-  return single_slab(g) && D <= g->ghost && D <= g->rows && D <= g->cols;
+  return D <= g->ghost && D <= g->rows && D <= g->cols;
 }
 
 // ---------------------------------------------------------------------------
@@ -576,7 +576,7 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
   for (int x = 0; x < 4; ++x)
     if (!lvl[x] || !aligned16(lvl[x])) return lvl[x] ? PS_ERR_ALIGN : PS_ERR_ARG;
   if ((s = check_table(g, t)) != PS_OK) return s;
-  if (tsteps != 1 && tsteps != 2 && tsteps != 4) return PS_ERR_ARG;
+  if (tsteps < 1 || tsteps > 4) return PS_ERR_ARG;
   if (tsteps > 1 && !tb_supported(g, t, tsteps)) return PS_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t k = 0;

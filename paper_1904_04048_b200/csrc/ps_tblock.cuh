@@ -1,5 +1,5 @@
 // ps_tblock.cuh — temporal blocking: TS two-step updates fused in one streaming pass
-// (BASELINE config 5, T in {2, 4}).  Included by ps_device.cu.
+// (BASELINE config 5, T in {2, 3, 4}).  Included by ps_device.cu.
 //
 // One pass reads u^k and u^{k-1} once and writes only the last two levels u^{k+TS-1}
 // and u^{k+TS}: HBM traffic falls from 3 words per update to 4/TS (+ halos).
@@ -34,6 +34,8 @@ struct TBParams {
   int32_t cmax;            // loadable columns: element index < cmax (from logical col 0)
   int32_t nstrips, rc, ntiles;
   int32_t reverse;         // walk tiles bottom-up (alternate launches: L2 reuse)
+  int32_t row_images;      // periodic: 1 = single slab, also write wrapped row images;
+                           // 0 = row slab of a ring (row halos come from the neighbours)
   // row slabs with in-kernel halo delivery (logical-origin pointers of the neighbours'
   // out_prev / out_last levels, null = none): out_last rows [0, R*TS) also land in the
   // slab above at rows up_rows + r, rows [rows - R*TS, rows) in the slab below at r - rows;
@@ -416,14 +418,15 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
     if constexpr (PER) {
       // refresh wrap-around images to depth D = R*TS (what the next pass loads)
       const int D = R * TS;
-      const bool erow = (row < D) || (row >= p.rows - D);
+      const int ri = p.row_images;
+      const bool erow = ri && ((row < D) || (row >= p.rows - D));
       const bool ecol = (gc0 < D) || (gc0 + V > p.cols - D);
       if (erow || ecol) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const int j = gc0 + v;
           if (j >= p.cols) continue;
-          for (int a = -1; a <= 1; ++a)
+          for (int a = -ri; a <= ri; ++a)
             for (int b = -1; b <= 1; ++b) {
               if (a == 0 && b == 0) continue;
               const int ii = row + a * p.rows;

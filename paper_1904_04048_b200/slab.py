@@ -7,12 +7,20 @@ they land in the ghost padding rows (-r..-1 / rows..rows+r-1) the kernels alread
 Per-point arithmetic is unchanged, so results are bitwise independent of P.
 
 * :func:`partition`, :class:`SlabPlan` — pure host logic (who owns which rows, which
-  rows go where), shared by every transport.
+  rows go where), shared by every transport.  Dirichlet grids are a line of slabs,
+  periodic grids a ring (rank 0 <-> rank P-1; columns wrap locally inside each slab).
 * :class:`VirtualSlabs` — P slabs on ONE device, halo rows moved by device copies.
   Tests the decomposition bit for bit without more GPUs.
 * :class:`DistributedSlabs` — one slab per rank (torchrun, one process per GPU),
   halo rows exchanged with NCCL send/recv on a communication stream while the
-  interior rows update (boundary rows first, then exchange || interior).
+  interior rows update (boundary rows first, then exchange || interior), or stored
+  straight into the neighbours' ghost rows by the update kernel (``transport="p2p"``).
+  One pass (boundary launches, exchange, interior launch) can be captured into a CUDA
+  graph per level-rotation phase and replayed (``graph=True``).
+* ``march_errsum`` on both — run()'s per-step error sums (simulator.py:275-280) across
+  slabs: each slab sums its own rows in numpy's pairwise order on the device, the P
+  partial pairs are gathered and added in rank order, so the result is bitwise
+  deterministic for a fixed P.
 
 The reference has no parallel path; its spec permits row partitioning that is
 bitwise deterministic for a fixed partition count.
@@ -21,6 +29,7 @@ bitwise deterministic for a fixed partition count.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from typing import NamedTuple
 
 import numpy as np
 
@@ -41,12 +50,32 @@ def partition(grows: int, P: int) -> list[tuple[int, int]]:
     return out
 
 
+class HaloMsg(NamedTuple):
+    """One halo message of a slab.  ``side`` names MY neighbour ("up" = the slab holding
+    the rows above mine); ``first``/``rows`` are my local rows sent, or my ghost rows
+    filled (negative = above row 0).  ``tag`` pairs a send with its recv when both
+    neighbours are the same rank (a periodic ring of two slabs)."""
+
+    peer: int
+    first: int
+    rows: int
+    side: str
+    tag: int
+
+
+UPWARD, DOWNWARD = 1, 2     # direction a message travels (towards lower / higher rows)
+
+
 @dataclass(frozen=True)
 class SlabPlan:
-    """Halo traffic of one slab: ``sends``/``recvs`` are (peer, first_local_row, nrows).
+    """Halo traffic of one slab.
 
-    A send of local rows [a, a+r) to ``peer`` pairs with that peer's recv into its
-    ghost rows.  Dirichlet grids are a line (no wrap); periodic grids are a ring."""
+    A send of my top rows travels upward into the upper neighbour's bottom ghost rows; a
+    send of my bottom rows travels downward into the lower neighbour's top ghost rows.
+    ``recvs`` are listed in the order the matching sends are issued on the peer (upward
+    message first), so a transport that matches messages between one pair of ranks by
+    issue order (NCCL) pairs them correctly even when up == down.  Dirichlet grids are a
+    line (no wrap); periodic grids are a ring."""
 
     rank: int
     P: int
@@ -55,8 +84,8 @@ class SlabPlan:
     halo: int
     up: int | None
     down: int | None
-    sends: tuple[tuple[int, int, int], ...]
-    recvs: tuple[tuple[int, int, int], ...]
+    sends: tuple[HaloMsg, ...]
+    recvs: tuple[HaloMsg, ...]
 
     @staticmethod
     def build(grows: int, P: int, rank: int, halo: int, periodic: bool) -> "SlabPlan":
@@ -68,51 +97,81 @@ class SlabPlan:
         down = rank + 1 if rank < P - 1 else (0 if periodic and P > 1 else None)
         sends, recvs = [], []
         if up is not None:
-            sends.append((up, 0, halo))              # my top rows -> up's bottom ghosts
-            recvs.append((up, -halo, halo))          # up's bottom rows -> my top ghosts
+            sends.append(HaloMsg(up, 0, halo, "up", UPWARD))
         if down is not None:
-            sends.append((down, rows - halo, halo))  # my bottom rows -> down's top ghosts
-            recvs.append((down, rows, halo))         # down's top rows -> my bottom ghosts
+            sends.append(HaloMsg(down, rows - halo, halo, "down", DOWNWARD))
+            recvs.append(HaloMsg(down, rows, halo, "down", UPWARD))      # its top rows
+        if up is not None:
+            recvs.append(HaloMsg(up, -halo, halo, "up", DOWNWARD))       # its bottom rows
         return SlabPlan(rank, P, row0, rows, halo, up, down, tuple(sends), tuple(recvs))
+
+    def send_rows(self, msg: HaloMsg, count: int) -> int:
+        """First local row of a ``count``-row send of ``msg``'s kind."""
+        return 0 if msg.side == "up" else self.rows - count
+
+    def recv_rows(self, msg: HaloMsg, count: int) -> int:
+        """First (ghost) row a ``count``-row recv of ``msg``'s kind fills."""
+        return -count if msg.side == "up" else self.rows
 
 
 def rows_view(level: nat.Level, first: int, count: int):
     """Flat torch view of ``count`` full-pitch rows starting at logical row ``first``
-    (may be negative: ghost rows).  Rows are contiguous in the padded layout."""
+    (may be negative: ghost rows).  Rows are contiguous in the padded layout; a periodic
+    slab's rows carry their wrap-around column images in the padding."""
     g = level.grid
     flat = level.buf.view(level.view().dtype)
     start = (g.ghost + first) * g.pitch
     return flat[start:start + count * g.pitch]
 
 
+def _check_common(transport, transports, tsteps, bc):
+    if transport not in transports:
+        raise ValueError(f"transport must be one of {transports}, got {transport!r}")
+    if tsteps not in (1, 2, 3, 4):
+        raise ValueError(f"tsteps must be 1, 2, 3 or 4, got {tsteps}")
+    if bc not in ("dirichlet", "periodic"):
+        raise ValueError(f"bc must be 'dirichlet' or 'periodic', got {bc!r}")
+
+
+def combine_partials(parts: np.ndarray) -> np.ndarray:
+    """(P, nsteps, 2) per-slab error sums -> (nsteps, 2), added in rank order
+    (left to right from slab 0): deterministic for a fixed P."""
+    total = np.array(parts[0], dtype=np.float64, copy=True)
+    for p in range(1, parts.shape[0]):
+        total = total + parts[p]
+    return total
+
+
 class VirtualSlabs:
-    """P Dirichlet row slabs of one (n+1)^2 grid on one device (test vehicle).
+    """P row slabs of one grid on one device (test vehicle): Dirichlet (n+1)^2 nodes as a
+    line of slabs, or periodic n^2 nodes as a ring.
 
     ``transport="copy"`` moves halo rows with device copies after each step;
-    ``transport="kernel"`` has each slab's update kernel store its boundary rows straight
-    into the neighbours' ghost rows (``ps_two_step_halo``) — the same code path the
-    multi-GPU p2p transport drives with peer-mapped pointers."""
+    ``transport="kernel"`` (Dirichlet) has each slab's update kernel store its boundary
+    rows straight into the neighbours' ghost rows (``ps_two_step_halo``) — the same code
+    path the multi-GPU p2p transport drives with peer-mapped pointers."""
 
     def __init__(self, scheme, n: int, lam: float, P: int, ring: int | None = None,
                  dtype: str = "f64", arith: str = "ref", c: float = 1.0,
-                 transport: str = "copy", tsteps: int = 1):
-        if transport not in ("copy", "kernel"):
-            raise ValueError(f"transport must be 'copy' or 'kernel', got {transport!r}")
-        if tsteps not in (1, 2, 4):
-            raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
-        self.transport = transport
+                 transport: str = "copy", tsteps: int = 1, bc: str = "dirichlet"):
+        _check_common(transport, ("copy", "kernel"), tsteps, bc)
+        if bc == "periodic" and transport == "kernel":
+            raise ValueError("in-kernel halo delivery serves Dirichlet slabs only")
+        self.transport, self.bc = transport, bc
         self.T = int(tsteps)
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         self.n, self.lam, self.P = int(n), float(lam), int(P)
         self.tau = self.lam / self.n / c
         R = self.spec.radius
         self.R = R
-        self.ring = R if ring is None else int(ring)
-        grows = self.n + 1
+        per = bc == "periodic"
+        self.ring = 0 if per else (R if ring is None else int(ring))
+        grows = self.n if per else self.n + 1
+        self.grows = grows
         H = R * self.T
-        self.plans = [SlabPlan.build(grows, P, p, H, periodic=False) for p in range(P)]
+        self.plans = [SlabPlan.build(grows, P, p, H, periodic=per) for p in range(P)]
         self.grids = [nat.make_slab_grid(grows, grows, pl.row0, pl.rows, max(2, H), self.ring,
-                                         "dirichlet", dtype, arith) for pl in self.plans]
+                                         bc, dtype, arith) for pl in self.plans]
         self.levels = [[nat.Level(g) for _ in range(3 if self.T == 1 else 4)]
                        for g in self.grids]
         self.previous = None
@@ -120,26 +179,38 @@ class VirtualSlabs:
         self.t_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
         self.t_two = nat.make_table(evaluate_table(self.spec.two_step, self.lam))
         self.newest = None
+        self._err = None
 
     def _exchange(self, idx: int, count: int | None = None):
         for p, pl in enumerate(self.plans):
-            for peer, first, halo in pl.sends:
-                k = halo if count is None else count
-                src_first = 0 if first == 0 else pl.rows - k
-                dst_first = -k if peer > p else self.plans[peer].rows
-                rows_view(self.levels[peer][idx], dst_first, k).copy_(
-                    rows_view(self.levels[p][idx], src_first, k))
+            for msg in pl.sends:
+                k = msg.rows if count is None else count
+                peer_plan = self.plans[msg.peer]
+                # my "up" send is the peer's recv from its "down" neighbour, and vice versa
+                dst_first = peer_plan.rows if msg.side == "up" else -k
+                rows_view(self.levels[msg.peer][idx], dst_first, k).copy_(
+                    rows_view(self.levels[p][idx], pl.send_rows(msg, k), k))
+
+    def _own(self, a: np.ndarray, pl: SlabPlan) -> np.ndarray:
+        rows = a[pl.row0:pl.row0 + pl.rows]
+        return rows[:, :self.grows] if self.bc == "periodic" else rows
 
     def load_initial(self, u0: np.ndarray, v0: np.ndarray):
+        """u0 / v0 in the reference's (n+1)^2 layout (periodic: alias row/col ignored)."""
         for pl, lv in zip(self.plans, self.levels):
-            lv[1].upload(u0[pl.row0:pl.row0 + pl.rows])
-            lv[0].upload(v0[pl.row0:pl.row0 + pl.rows])
+            lv[1].upload(self._own(u0, pl))
+            lv[0].upload(self._own(v0, pl))
+            if self.bc == "periodic":     # column images; the exchange brings the row halos
+                lv[1].fill_ghosts()
+                lv[0].fill_ghosts()
         self._exchange(1)
         self._exchange(0)
 
     def first_step(self):
         for g, lv in zip(self.grids, self.levels):
             nat.first_step(g, lv[1], lv[0], lv[2], self.t_u, self.t_v, self.tau)
+            if self.bc == "periodic" and self.T > 1:
+                lv[2].fill_ghosts()       # column images to the blocked passes' depth R*T
         self._exchange(2)
         self.newest, self.previous = 2, 1
 
@@ -169,50 +240,99 @@ class VirtualSlabs:
                 self._exchange(f1, R * (T - 1))
             self.newest, self.previous = f2, f1
 
+    def _step(self):
+        cur = self.newest
+        nxt, prev = (cur + 1) % 3, (cur + 2) % 3
+        R = self.R
+        for p, (g, lv) in enumerate(zip(self.grids, self.levels)):
+            if self.transport == "copy":
+                nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
+                continue
+            up = self.levels[p - 1][nxt].ptr.value if p > 0 else None
+            dn = self.levels[p + 1][nxt].ptr.value if p + 1 < self.P else None
+            up_rows = self.plans[p - 1].rows if p > 0 else 0
+            nat.two_step_halo(g, lv[cur], lv[prev], lv[nxt], self.t_two, 0, g.rows, up,
+                              up_rows, dn)
+        if self.transport == "copy":
+            self._exchange(nxt, R)
+        self.newest, self.previous = nxt, cur
+
     def march(self, nsteps: int):
         if self.T > 1:
             self._march_blocked(nsteps)
             return
         for _ in range(nsteps):
-            cur = self.newest
-            nxt, prev = (cur + 1) % 3, (cur + 2) % 3
-            R = self.R
-            for p, (g, lv) in enumerate(zip(self.grids, self.levels)):
-                if self.transport == "copy":
-                    nat.two_step(g, lv[cur], lv[prev], lv[nxt], self.t_two)
-                    continue
-                up = self.levels[p - 1][nxt].ptr.value if p > 0 else None
-                dn = self.levels[p + 1][nxt].ptr.value if p + 1 < self.P else None
-                up_rows = self.plans[p - 1].rows if p > 0 else 0
-                nat.two_step_halo(g, lv[cur], lv[prev], lv[nxt], self.t_two, 0, g.rows, up,
-                                  up_rows, dn)
-            if self.transport == "copy":
-                self._exchange(nxt, R)
-            self.newest, self.previous = nxt, cur
+            self._step()
+
+    # -- run()'s error metric across slabs ------------------------------
+    def _err_rows(self, p: int) -> int:
+        """Rows of the reference's (n+1)^2 array slab p accounts for (periodic: the last
+        slab also owns the alias row n, which its bottom ghost row holds)."""
+        extra = 1 if self.bc == "periodic" and p == self.P - 1 else 0
+        return self.plans[p].rows + extra
+
+    def load_reference_shape(self, S: np.ndarray):
+        """S = sin(2πx1) sin(2πx2) on the (n+1)^2 nodes, as numpy computes it (the static
+        factor of the default standing wave); kept per slab in level layout."""
+        import torch
+
+        self._S = []
+        for p, (pl, g) in enumerate(zip(self.plans, self.grids)):
+            lv = nat.Level(g)
+            rows = self._err_rows(p)
+            lv.upload(np.ascontiguousarray(S[pl.row0:pl.row0 + rows, :self.n + 1]))
+            self._S.append(lv)
+        self._err = [nat.ErrSum(self._err_rows(p), self.n + 1) for p in range(self.P)]
+        self._err_out = torch.zeros(2, dtype=torch.float64, device="cuda")
+
+    def march_errsum(self, st: np.ndarray) -> np.ndarray:
+        """len(st) single steps (T = 1), each followed by the error sums against S*st[k];
+        returns (nsteps, 2): sum((u - ref)^2), sum(ref^2), partials added in slab order."""
+        import torch
+
+        if self.T != 1 or self._err is None:
+            raise RuntimeError("march_errsum needs tsteps=1 and load_reference_shape()")
+        parts = torch.zeros((self.P, len(st), 2), dtype=torch.float64, device="cuda")
+        for k, s in enumerate(st):
+            self._step()
+            for p in range(self.P):
+                self._err[p].step(self.grids[p], self.levels[p][self.newest], self._S[p],
+                                  float(s), parts[p, k].data_ptr())
+        return combine_partials(parts.cpu().numpy())
 
     def field(self) -> np.ndarray:
-        return np.concatenate([lv[self.newest].download() for lv in self.levels], axis=0)
+        core = np.concatenate([lv[self.newest].download() for lv in self.levels], axis=0)
+        if self.bc != "periodic":
+            return core
+        out = np.empty((self.n + 1, self.n + 1), dtype=core.dtype)
+        out[:self.n, :self.n] = core
+        out[self.n, :self.n] = core[0]
+        out[:, self.n] = out[:, 0]
+        return out
 
 
 class DistributedSlabs:
-    """This rank's Dirichlet row slab of an (n+1)^2 grid; halo exchange over
+    """This rank's row slab of a Dirichlet (n+1)^2 or periodic n^2 grid; halo exchange over
     ``torch.distributed`` (NCCL on GPUs) overlapped with the interior update.
 
     ``compute`` supplies the per-slab updates (``first_step(grid, u0, v0, out)`` and
     ``two_step_rows(grid, uk, ukm1, out, lo, hi)``); the default is libps.so's kernels.
     The multi-process CPU tests substitute a host implementation to check the
-    exchange logic under gloo."""
+    exchange logic under gloo.  Under a gloo group device levels still work: halo rows
+    are staged through host memory and the p2p transport's ordering tokens travel as CPU
+    tensors after a stream synchronisation (two processes sharing one GPU in the tests;
+    NCCL cannot place two ranks on one device)."""
 
     def __init__(self, scheme, n: int, lam: float, ring: int | None = None, dtype: str = "f64",
                  arith: str = "ref", c: float = 1.0, group=None, device=None, compute=None,
-                 level_factory=None, transport: str = "nccl", tsteps: int = 1):
+                 level_factory=None, transport: str = "nccl", tsteps: int = 1,
+                 bc: str = "dirichlet", graph: bool = False):
         import torch.distributed as dist
 
-        if transport not in ("nccl", "p2p"):
-            raise ValueError(f"transport must be 'nccl' or 'p2p', got {transport!r}")
-        if tsteps not in (1, 2, 4):
-            raise ValueError(f"tsteps must be 1, 2 or 4, got {tsteps}")
-        self.transport = transport
+        _check_common(transport, ("nccl", "p2p"), tsteps, bc)
+        if bc == "periodic" and transport == "p2p":
+            raise ValueError("in-kernel halo delivery serves Dirichlet slabs only")
+        self.transport, self.bc = transport, bc
         # Temporal blocking depth T: one pass advances T steps, so the halo is R*T rows of
         # the newest level and R*(T-1) rows of the one before (SURVEY.md §8e E4).
         self.T = int(tsteps)
@@ -220,24 +340,32 @@ class DistributedSlabs:
         self.group = group
         self.rank = dist.get_rank(group)
         self.P = dist.get_world_size(group)
+        self.host_staged = dist.get_backend(group) != "nccl"
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         self.n, self.lam = int(n), float(lam)
         self.tau = self.lam / self.n / c
         R = self.spec.radius
         self.R = R
-        self.ring = R if ring is None else int(ring)
-        grows = self.n + 1
+        per = bc == "periodic"
+        self.ring = 0 if per else (R if ring is None else int(ring))
+        grows = self.n if per else self.n + 1
         self.grows = grows
-        self.plan = SlabPlan.build(grows, self.P, self.rank, R * self.T, periodic=False)
+        self.plan = SlabPlan.build(grows, self.P, self.rank, R * self.T, periodic=per)
         self.grid = nat.make_slab_grid(grows, grows, self.plan.row0, self.plan.rows,
-                                       max(2, R * self.T), self.ring, "dirichlet", dtype, arith)
+                                       max(2, R * self.T), self.ring, bc, dtype, arith)
         make = level_factory or (lambda g: nat.Level(g, device=device))
+        self._make_level = make
         self.levels = [make(self.grid) for _ in range(3 if self.T == 1 else 4)]
         self.previous = None
         self.compute = compute or _KernelCompute(self.spec, self.lam, self.tau)
         self.newest = None
         self._streams = None
         self._peer = None
+        self._want_graph = bool(graph) and self.compute.is_cuda
+        self._graphs = {}
+        self.graphed = False     # True once a pass has been replayed from a CUDA graph
+        self.graph_error = None
+        self._err = None
         if transport == "p2p":
             self._open_peers()
 
@@ -263,22 +391,30 @@ class DistributedSlabs:
         self._peer = peer
         import torch
 
-        self._tok = torch.zeros(4, dtype=torch.int32, device=self.levels[0].buf.device)
+        dev = "cpu" if self.host_staged else self.levels[0].buf.device
+        self._tok = torch.zeros(4, dtype=torch.int32, device=dev)
 
-    def _token_exchange(self):
+    def _token_exchange(self, edge_event=None):
         """Tiny send/recv with each neighbour: orders my next step after their boundary
-        kernels (whose stores into my ghost rows then have landed)."""
+        kernels (whose stores into my ghost rows then have landed).  NCCL tokens are
+        stream-ordered; host tokens (gloo) are sent once my own boundary kernels have
+        completed (``edge_event``) and received before the next launches are queued."""
         ops = []
         t = self._tok
-        for i, (peer, _, _) in enumerate(self.plan.recvs):
-            ops.append(self.dist.P2POp(self.dist.irecv, t[i:i + 1], peer, self.group))
-        for i, (peer, _, _) in enumerate(self.plan.sends):
-            ops.append(self.dist.P2POp(self.dist.isend, t[2 + i:3 + i], peer, self.group))
+        if self.host_staged and edge_event is not None:
+            edge_event.synchronize()
+        for i, msg in enumerate(self.plan.recvs):
+            ops.append(self.dist.P2POp(self.dist.irecv, t[i:i + 1], msg.peer, self.group,
+                                       msg.tag))
+        for i, msg in enumerate(self.plan.sends):
+            ops.append(self.dist.P2POp(self.dist.isend, t[2 + i:3 + i], msg.peer, self.group,
+                                       msg.tag))
         if ops:
             for w in self.dist.batch_isend_irecv(ops):
                 w.wait()
 
     def close(self):
+        self._graphs.clear()
         if self._peer:
             for base in self._peer["opened"]:
                 try:
@@ -288,132 +424,205 @@ class DistributedSlabs:
             self._peer = None
 
     # -- transport ---------------------------------------------------------------------
-    def _p2p_ops(self, idx: int, count: int):
-        """Send my first/last ``count`` rows of level ``idx`` up/down; receive the
-        neighbours' into my ghost rows."""
-        ops = []
+    def _halo_msgs(self, idx: int, count: int):
+        """(is_send, view, msg) of a ``count``-row exchange of level ``idx``."""
         lv = self.levels[idx]
-        rows = self.plan.rows
-        for peer, first, _ in self.plan.recvs:
-            dst = -count if first < 0 else rows
-            ops.append(self.dist.P2POp(self.dist.irecv, rows_view(lv, dst, count), peer,
-                                       self.group))
-        for peer, first, _ in self.plan.sends:
-            src = 0 if first == 0 else rows - count
-            ops.append(self.dist.P2POp(self.dist.isend, rows_view(lv, src, count), peer,
-                                       self.group))
-        return ops
+        out = [(False, rows_view(lv, self.plan.recv_rows(m, count), count), m)
+               for m in self.plan.recvs]
+        out += [(True, rows_view(lv, self.plan.send_rows(m, count), count), m)
+                for m in self.plan.sends]
+        return out
 
     def exchange(self, idx: int, count: int | None = None, idx2: int | None = None,
                  count2: int = 0):
         """Blocking (w.r.t. the current stream) halo exchange of level ``idx`` (``count``
         rows; default the full halo) and optionally ``count2`` rows of level ``idx2``."""
-        ops = self._p2p_ops(idx, self.plan.halo if count is None else count)
+        msgs = self._halo_msgs(idx, self.plan.halo if count is None else count)
         if idx2 is not None and count2 > 0:
-            ops += self._p2p_ops(idx2, count2)
-        if ops:
-            for w in self.dist.batch_isend_irecv(ops):
-                w.wait()
+            msgs += self._halo_msgs(idx2, count2)
+        if not msgs:
+            return
+        stage = self.host_staged and msgs[0][1].is_cuda
+        ops, landed = [], []
+        for is_send, view, m in msgs:
+            buf = view
+            if stage:      # gloo moves CPU tensors: stage the rows through host memory
+                buf = view.cpu() if is_send else view.new_empty(view.shape, device="cpu")
+                if not is_send:
+                    landed.append((view, buf))
+            ops.append(self.dist.P2POp(self.dist.isend if is_send else self.dist.irecv, buf,
+                                       m.peer, self.group, m.tag))
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
+        for view, buf in landed:
+            view.copy_(buf)
 
     # -- time stepping -------------------------------------------------------------------
     def load_initial(self, u0_rows: np.ndarray, v0_rows: np.ndarray):
-        """Upload this slab's own rows of u0 / v0, then exchange their halos."""
+        """Upload this slab's own rows of u0 / v0 (periodic: the n core columns), then
+        exchange their halos."""
         self.levels[1].upload(u0_rows)
         self.levels[0].upload(v0_rows)
+        if self.bc == "periodic":
+            self.levels[1].fill_ghosts()
+            self.levels[0].fill_ghosts()
         self.exchange(1)
         self.exchange(0)
 
     def first_step(self):
         self.compute.first_step(self.grid, self.levels[1], self.levels[0], self.levels[2])
+        if self.bc == "periodic" and self.T > 1:
+            self.levels[2].fill_ghosts()
         self.exchange(2)
         self.newest, self.previous = 2, 1
 
-    def step(self, overlap: bool = True):
+    def _overlapped(self, rows: int, depth: int, overlap: bool) -> bool:
+        return not (self.P == 1 or rows < 3 * depth or not overlap or not self.compute.is_cuda)
+
+    def _streams_events(self):
+        import torch
+
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
+        return self._streams
+
+    def _step_body(self, cur: int, prev: int, nxt: int, overlap: bool):
         """One two-step update: boundary rows, then halo exchange on the communication
         stream concurrently with the interior rows."""
-        if self.T > 1:
-            raise RuntimeError("temporally blocked slabs advance with step_block()/march()")
-        cur = self.newest
-        nxt, prev = (cur + 1) % 3, (cur + 2) % 3
         lv = self.levels
         rows, R = self.plan.rows, self.R
         c = self.compute
-        if self.P == 1 or rows < 3 * R or not overlap or not c.is_cuda:
+        if not self._overlapped(rows, R, overlap):
             c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, rows)
             self.exchange(nxt)
+            return
+        import torch
+
+        comm, ev_edge, ev_comm = self._streams_events()
+        main = torch.cuda.current_stream()
+        if self.transport == "p2p":
+            # boundary rows land in the neighbours' ghost rows from inside the kernel
+            pr = self._peer
+            up = pr["up"][nxt] if pr["up"] else None
+            dn = pr["dn"][nxt] if pr["dn"] else None
+            c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], 0, R, up, pr["up_rows"], dn)
+            c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows, up,
+                            pr["up_rows"], dn)
         else:
-            import torch
-
-            if self._streams is None:
-                self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
-            comm, ev_edge, ev_comm = self._streams
-            main = torch.cuda.current_stream()
-            if self.transport == "p2p":
-                # boundary rows land in the neighbours' ghost rows from inside the kernel
-                pr = self._peer
-                up = pr["up"][nxt] if pr["up"] else None
-                dn = pr["dn"][nxt] if pr["dn"] else None
-                c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], 0, R, up, pr["up_rows"],
-                                dn)
-                c.two_step_halo(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows, up,
-                                pr["up_rows"], dn)
-            else:
-                c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, R)
-                c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows)
-            ev_edge.record(main)
-            with torch.cuda.stream(comm):
-                comm.wait_event(ev_edge)
-                if self.transport == "p2p":
-                    self._token_exchange()
-                else:
-                    self.exchange(nxt)
-                ev_comm.record(comm)
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], 0, R)
+            c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], rows - R, rows)
+        ev_edge.record(main)
+        if self.host_staged:
+            # host-side transport: queue the interior first, then talk to the neighbours
             c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], R, rows - R)
-            main.wait_event(ev_comm)
-        self.newest, self.previous = nxt, cur
+            if self.transport == "p2p":
+                self._token_exchange(ev_edge)
+            else:
+                self.exchange(nxt)
+            return
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev_edge)
+            if self.transport == "p2p":
+                self._token_exchange()
+            else:
+                self.exchange(nxt)
+            ev_comm.record(comm)
+        c.two_step_rows(self.grid, lv[cur], lv[prev], lv[nxt], R, rows - R)
+        main.wait_event(ev_comm)
 
-    def step_block(self, overlap: bool = True):
+    def _block_body(self, cur: int, prev: int, f1: int, f2: int, overlap: bool):
         """One temporally blocked pass: T updates.  Boundary rows (R*T each side) first,
         then their halo rows of the two newest levels go to the neighbours on the
         communication stream while the interior rows update."""
         T, R, rows = self.T, self.R, self.plan.rows
-        cur, prev = self.newest, self.previous
-        f1, f2 = [x for x in range(4) if x not in (cur, prev)]
         lv, c = self.levels, self.compute
         H = R * T
-        if self.P == 1 or rows < 3 * H or not overlap or not c.is_cuda:
+        if not self._overlapped(rows, H, overlap):
             c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, rows)
             self.exchange(f2, H, f1, R * (T - 1))   # (p2p slabs too: plain copy here)
-        else:
-            import torch
+            return
+        import torch
 
-            if self._streams is None:
-                self._streams = (torch.cuda.Stream(), torch.cuda.Event(), torch.cuda.Event())
-            comm, ev_edge, ev_comm = self._streams
-            main = torch.cuda.current_stream()
-            if self.transport == "p2p":
-                # the boundary passes store their rows of both output levels straight into
-                # the neighbours' ghost rows (peer memory); a token orders the next pass
-                pr = self._peer
-                up = (pr["up"][f1], pr["up"][f2]) if pr["up"] else None
-                dn = (pr["dn"][f1], pr["dn"][f2]) if pr["dn"] else None
-                c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H, up,
-                          pr["up_rows"], dn)
-                c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows, up,
-                          pr["up_rows"], dn)
-            else:
-                c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H)
-                c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows)
-            ev_edge.record(main)
-            with torch.cuda.stream(comm):
-                comm.wait_event(ev_edge)
-                if self.transport == "p2p":
-                    self._token_exchange()
-                else:
-                    self.exchange(f2, H, f1, R * (T - 1))
-                ev_comm.record(comm)
+        comm, ev_edge, ev_comm = self._streams_events()
+        main = torch.cuda.current_stream()
+        if self.transport == "p2p":
+            # the boundary passes store their rows of both output levels straight into
+            # the neighbours' ghost rows (peer memory); a token orders the next pass
+            pr = self._peer
+            up = (pr["up"][f1], pr["up"][f2]) if pr["up"] else None
+            dn = (pr["dn"][f1], pr["dn"][f2]) if pr["dn"] else None
+            c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H, up,
+                      pr["up_rows"], dn)
+            c.tb_halo(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows, up,
+                      pr["up_rows"], dn)
+        else:
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, 0, H)
+            c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, rows - H, rows)
+        ev_edge.record(main)
+        if self.host_staged:
             c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, H, rows - H)
-            main.wait_event(ev_comm)
+            if self.transport == "p2p":
+                self._token_exchange(ev_edge)
+            else:
+                self.exchange(f2, H, f1, R * (T - 1))
+            return
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev_edge)
+            if self.transport == "p2p":
+                self._token_exchange()
+            else:
+                self.exchange(f2, H, f1, R * (T - 1))
+            ev_comm.record(comm)
+        c.tb_rows(self.grid, lv[cur], lv[prev], lv[f1], lv[f2], T, H, rows - H)
+        main.wait_event(ev_comm)
+
+    def _replay(self, key, body) -> bool:
+        """Run ``body`` (one pass) from a CUDA graph captured once per level-rotation
+        phase ``key``: kernels, NCCL send/recv and the cross-stream events of a pass
+        become one graph launch (no per-pass host launch cost).  Returns False — and stays
+        eager from then on — if capture is unavailable (host-staged transports, or the
+        capture failed)."""
+        if not self._want_graph or self.host_staged:
+            return False
+        import torch
+
+        g = self._graphs.get(key)
+        if g is None:
+            try:
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    body()
+                self._graphs[key] = g
+            except Exception as exc:  # capture is an optimisation, never a requirement
+                self.graph_error = f"{type(exc).__name__}: {exc}"
+                self._want_graph = False
+                self._streams = None
+                torch.cuda.synchronize()
+                return False
+            # capture records, it does not execute: replay below runs the pass
+        g.replay()
+        self.graphed = True
+        return True
+
+    def step(self, overlap: bool = True):
+        """One two-step update (T = 1)."""
+        if self.T > 1:
+            raise RuntimeError("temporally blocked slabs advance with step_block()/march()")
+        cur = self.newest
+        nxt, prev = (cur + 1) % 3, (cur + 2) % 3
+        if not self._replay(("s", cur, overlap),
+                            lambda: self._step_body(cur, prev, nxt, overlap)):
+            self._step_body(cur, prev, nxt, overlap)
+        self.newest, self.previous = nxt, cur
+
+    def step_block(self, overlap: bool = True):
+        """One temporally blocked pass of T updates."""
+        cur, prev = self.newest, self.previous
+        f1, f2 = [x for x in range(4) if x not in (cur, prev)]
+        if not self._replay(("b", cur, prev, overlap),
+                            lambda: self._block_body(cur, prev, f1, f2, overlap)):
+            self._block_body(cur, prev, f1, f2, overlap)
         self.newest, self.previous = f2, f1
 
     def march(self, nsteps: int, overlap: bool = True):
@@ -425,6 +634,46 @@ class DistributedSlabs:
             raise ValueError(f"nsteps={nsteps} must be a multiple of tsteps={self.T}")
         for _ in range(nsteps // self.T):
             self.step_block(overlap)
+
+    # -- run()'s error metric across slabs ------------------------------
+    def err_rows(self) -> int:
+        """Rows of the reference's (n+1)^2 array this slab accounts for (periodic: the
+        last slab also owns the alias row n, held by its bottom ghost row)."""
+        extra = 1 if self.bc == "periodic" and self.rank == self.P - 1 else 0
+        return self.plan.rows + extra
+
+    def load_reference_shape(self, S_rows: np.ndarray):
+        """This slab's ``err_rows()`` rows (all n+1 columns) of S = sin(2πx1) sin(2πx2),
+        the static factor of the default standing wave, as numpy computes it."""
+        S_rows = np.ascontiguousarray(S_rows)
+        if S_rows.shape != (self.err_rows(), self.n + 1):
+            raise ValueError(f"S_rows must be {(self.err_rows(), self.n + 1)}, got {S_rows.shape}")
+        self._S = self._make_level(self.grid)
+        self._S.upload(S_rows)
+        self._err = self.compute.errsum_plan(self.err_rows(), self.n + 1)
+
+    def march_errsum(self, st, overlap: bool = True) -> np.ndarray:
+        """len(st) single steps (T = 1), each followed by this slab's error sums against
+        S*st[k] in numpy's pairwise order; the P partial pairs per step are gathered once
+        at the end and added in rank order on every rank, so all ranks return the same
+        (nsteps, 2) array of sum((u - ref)^2), sum(ref^2), bitwise deterministic for a
+        fixed P (replaces simulator.py:275-280)."""
+        import torch
+
+        if self.T != 1 or self._err is None:
+            raise RuntimeError("march_errsum needs tsteps=1 and load_reference_shape()")
+        st = np.asarray(st, dtype=np.float64)
+        dev = self.levels[0].buf.device
+        mine = torch.zeros((len(st), 2), dtype=torch.float64, device=dev)
+        for k, s in enumerate(st):
+            self.step(overlap)
+            self.compute.errsum(self._err, self.grid, self.levels[self.newest], self._S,
+                                float(s), mine[k])
+        if self.host_staged:
+            mine = mine.cpu()
+        parts = [torch.zeros_like(mine) for _ in range(self.P)]
+        self.dist.all_gather(parts, mine, group=self.group)
+        return combine_partials(np.stack([p.cpu().numpy() for p in parts]))
 
     def own_rows(self, which: str = "newest") -> np.ndarray:
         idx = self.newest if which == "newest" else self.previous
@@ -461,3 +710,9 @@ class _KernelCompute:
         if hi > lo:
             nat.two_step_tb_halo(grid, uk, ukm1, out_prev, out_last, self.t_two, T, lo, hi, up,
                                  up_rows, dn)
+
+    def errsum_plan(self, rows_h, cols_h):
+        return nat.ErrSum(rows_h, cols_h)
+
+    def errsum(self, plan, grid, level, S, st, out2):
+        plan.step(grid, level, S, st, out2.data_ptr())
