@@ -363,6 +363,7 @@ class DistributedSlabs:
         self._peer = None
         self._want_graph = bool(graph) and self.compute.is_cuda
         self._graphs = {}
+        self._seen = set()
         self.graphed = False     # True once a pass has been replayed from a CUDA graph
         self.graph_error = None
         self._err = None
@@ -588,6 +589,11 @@ class DistributedSlabs:
 
         g = self._graphs.get(key)
         if g is None:
+            if key not in self._seen:
+                # the first pass of each phase runs eagerly (one-time kernel attribute
+                # set-up and NCCL channel warm-up happen outside any capture)
+                self._seen.add(key)
+                return False
             try:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()

@@ -360,7 +360,7 @@ def test_config4_full_size_slab_check(oracle):
 # ------------------------------------------------------------ temporal blocking (K3)
 @pytest.mark.parametrize("name,radius", SHAPES)
 @pytest.mark.parametrize("dtype,arith", [("f64", "ref"), ("f32", "ref"), ("f32", "native")])
-@pytest.mark.parametrize("tsteps", [2, 4])
+@pytest.mark.parametrize("tsteps", [2, 3, 4])
 @pytest.mark.parametrize("n", [45, 700, 2100])  # 2100: several column strips at every geometry
 @pytest.mark.parametrize("bc", ["dirichlet", "periodic"])
 def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps, n, bc, oracle):
@@ -510,6 +510,47 @@ def test_config5_full_size_blocking_is_bitwise():
         del sim
         torch.cuda.empty_cache()
     assert sums[2] == sums[1] and sums[4] == sums[1], sums
+
+
+def _full_size_checksums(scheme, n, lam, dtype, arith, gauss, tsteps, steps):
+    """Bit-pattern checksums of both live levels after `steps` march steps at depth tsteps."""
+    import torch
+
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation(scheme, n, lam, bc="dirichlet", dtype=dtype, arith=arith, tsteps=tsteps)
+    K, wmin, wmax, vzero = gauss
+    sim.gaussian_initial(K, wmin, wmax, seed=0, v_zero=vzero)
+    sim.first_step()
+    sim.march(steps)
+    out = (_checksum(sim.levels[sim.newest]), _checksum(sim.levels[sim.previous]))
+    del sim
+    torch.cuda.empty_cache()
+    return out
+
+
+def test_config4_full_size_blocking_is_bitwise():
+    """C4 at the benched geometry (P9, ring 1, 32768^2 f64, T=4: two 16-B vectors per lane,
+    8 warpgroup-specialised consumer warps, 256-row tiles): after 42 steps (10 fused
+    passes + 2 single steps) both live levels carry the T=1 march's bits."""
+    args = ("P9", 32767, 0.6, "f64", "ref", (64, 0.01, 0.05, True))
+    want = _full_size_checksums(*args, 1, 42)
+    assert _full_size_checksums(*args, 4, 42) == want
+    assert _full_size_checksums(*args, 2, 42) == want
+
+
+def test_config3_full_size_blocking_is_bitwise():
+    """C3 f64 at full size (P13, ring 2, 16384^2): T=2 (the benched depth), T=3 and T=4
+    marches equal the T=1 march bit for bit after 40 steps; the f32 reference contract
+    likewise at T=2."""
+    args = ("P13", 16383, 0.4, "f64", "ref", (32, 0.01, 0.05, False))
+    want = _full_size_checksums(*args, 1, 40)
+    for ts in (2, 3, 4):
+        assert _full_size_checksums(*args, ts, 40) == want, ts
+    args = ("P13", 16383, 0.4, "f32", "ref", (32, 0.01, 0.05, False))
+    assert _full_size_checksums(*args, 2, 40) == _full_size_checksums(*args, 1, 40)
+    args = ("P13", 16383, 0.4, "f32", "native", (32, 0.01, 0.05, False))
+    assert _full_size_checksums(*args, 4, 40) == _full_size_checksums(*args, 1, 40)
 
 
 def test_config5_full_size_f32_against_f64():
