@@ -22,6 +22,12 @@ struct Arith<double, A> {
   __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, double u) {
     return __dadd_rn(acc, __dmul_rn(c, u));
   }
+  // tap() in two halves: the separately rounded product fl(c*u) — the same value for
+  // every output point that reads u through a tap with this coefficient, so the fused
+  // kernels compute it once per input element and coefficient class — and the add
+  static constexpr bool kSplit = true;
+  __device__ __forceinline__ static acc_t mul(coef_t c, double u) { return __dmul_rn(c, u); }
+  __device__ __forceinline__ static acc_t add(acc_t acc, acc_t p) { return __dadd_rn(acc, p); }
   // u^{k+1} = acc - u^{k-1}            (simulator.py:184)
   __device__ __forceinline__ static double two(acc_t acc, double ukm1) {
     return __dsub_rn(acc, ukm1);
@@ -48,6 +54,11 @@ struct Arith<float, ARITH_REF> {
   __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, float u) {
     return __dadd_rn(acc, static_cast<double>(__fmul_rn(c, u)));
   }
+  static constexpr bool kSplit = true;   // product = the f32 product widened once
+  __device__ __forceinline__ static acc_t mul(coef_t c, float u) {
+    return static_cast<double>(__fmul_rn(c, u));
+  }
+  __device__ __forceinline__ static acc_t add(acc_t acc, acc_t p) { return __dadd_rn(acc, p); }
   __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
     return __fsub_rn(__double2float_rn(acc), ukm1);
   }
@@ -72,6 +83,7 @@ struct Arith<float, ARITH_NATIVE> {
   __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, float u) {
     return __fmaf_rn(c, u, acc);
   }
+  static constexpr bool kSplit = false;  // one fused operation per tap: nothing to share
   __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
     return __fsub_rn(acc, ukm1);
   }

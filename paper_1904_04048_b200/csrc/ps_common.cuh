@@ -333,9 +333,17 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 // vs 1008: spills) and periodic grids (C2: 251 vs 324) stay at one vector.  Folding the
 // producer into consumer warp 0 (8 consumer warps, 2 per sub-partition) lost everywhere
 // (C4 528, C5 801).
-template <typename T, class S, int TS, bool PER>
+#ifndef PS_TB_SYM_VM
+#define PS_TB_SYM_VM 1   // vectors per lane of the shared-product kernels (state: 15 doubles
+#endif                   // per stage at one f64 vector, 27 at two: T=4 fits only with one)
+#ifndef PS_TB_SYM_WGS
+#define PS_TB_SYM_WGS 1  // shared-product kernels: 12 warpgroup-specialised consumer warps
+#endif
+template <typename T, int A, class S, int TS, bool PER>
 constexpr int tb_vm() {
-  return PS_TB_VM > 0 ? PS_TB_VM : ((sizeof(T) == 8 && S::R == 1 && !PER) ? 2 : 1);
+  return PS_TB_VM > 0            ? PS_TB_VM
+         : tb_sym<T, A, S, TS>()     ? PS_TB_SYM_VM
+                                 : ((sizeof(T) == 8 && S::R == 1 && !PER) ? 2 : 1);
 }
 #ifndef PS_TB_WGS
 #define PS_TB_WGS -1
@@ -347,18 +355,19 @@ constexpr int tb_vm() {
 #ifndef PS_TB_WGS1
 #define PS_TB_WGS1 -1  // one-vector geometries: 1 = always, 0 = never, -1 = f32 Dirichlet
 #endif
-template <typename T, class S, int TS, bool PER>
+template <typename T, int A, class S, int TS, bool PER>
 constexpr bool tb_wgs() {
   return PS_TB_WGS >= 0 ? PS_TB_WGS != 0
-         : tb_vm<T, S, TS, PER>() == 2
+         : tb_vm<T, A, S, TS, PER>() == 2
              ? true
-             : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0 : (sizeof(T) == 4 && !PER));
+             : (tb_sym<T, A, S, TS>() ? (PS_TB_SYM_WGS != 0 && !PER)
+                : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0 : (sizeof(T) == 4 && !PER)));
 }
-template <typename T, class S, int TS, bool PER>
+template <typename T, int A, class S, int TS, bool PER>
 constexpr int tb_nw() {
-  return tb_wgs<T, S, TS, PER>() ? (tb_vm<T, S, TS, PER>() == 2 ? 8 : 12)
-         : PS_TB_NW > 0          ? PS_TB_NW
-                                 : (tb_vm<T, S, TS, PER>() == 2 ? 7 : 11);
+  return tb_wgs<T, A, S, TS, PER>() ? (tb_vm<T, A, S, TS, PER>() == 2 ? 8 : 12)
+         : PS_TB_NW > 0             ? PS_TB_NW
+                                    : (tb_vm<T, A, S, TS, PER>() == 2 ? 7 : 11);
 }
 template <typename T, int TS>
 constexpr int tb_ns() {
@@ -369,13 +378,16 @@ template <typename T, int A, class S, int TS, bool PER, bool HALO>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
-  constexpr int VM = tb_vm<T, S, TS, PER>(), NW = tb_nw<T, S, TS, PER>(), NS = tb_ns<T, TS>();
-  constexpr bool WGS = tb_wgs<T, S, TS, PER>();
+  constexpr int VM = tb_vm<T, A, S, TS, PER>(), NW = tb_nw<T, A, S, TS, PER>(), NS = tb_ns<T, TS>();
+  constexpr bool WGS = tb_wgs<T, A, S, TS, PER>();
+  constexpr bool SYM = tb_sym<T, A, S, TS>();
+  if (SYM && !tb_classes_equal<S>(t)) return PS_ERR_TABLE;  // (tb_supported screens these)
   constexpr int NT = (NW + (WGS ? 4 : 1)) * 32;  // threads per block (consumers + producer)
   // rows per pipeline slot: one window rotation (2R+1) for radius 1; radius 2 takes 6
   // (measured: C5 1052 -> 1080, C3 f32 827 -> 837 GLUP/s; fewer ring waits per row, and
   // 8 or 10 rows no longer fit the shared memory)
-  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : (S::R == 2 ? 6 : 2 * S::R + 1);
+  // shared-product kernels rotate 2R-row delay lines: a multiple of 2R rows per slot
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? 4 : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
   static std::once_flag once[kMaxDevices];

@@ -134,6 +134,17 @@ static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
   const bool shape = shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) ||
                      shape_matches<ShapeC9>(t) || shape_matches<ShapeP13>(t);
   if (!shape || g->rows < 4 || g->cols < 4) return false;
+  // the reference-contract fused kernels share one product per input element and
+  // coefficient class (ps_tblock.cuh): the table must give each class one coefficient
+  // (every named scheme does); others run unblocked
+  const bool ref = g->dtype == PS_F64 || g->arith == PS_ARITH_REF;
+  if (ref && PS_TB_SYM != 0 && (table_radius(t) == 1 || tsteps <= PS_TB_SYM_R2_MAXT)) {
+    const bool eq = shape_matches<ShapeP5>(t)   ? tb_classes_equal<ShapeP5>(t)
+                    : shape_matches<ShapeP9>(t) ? tb_classes_equal<ShapeP9>(t)
+                    : shape_matches<ShapeC9>(t) ? tb_classes_equal<ShapeC9>(t)
+                                                : tb_classes_equal<ShapeP13>(t);
+    if (!eq) return false;
+  }
   if (g->bc == PS_BC_DIRICHLET) return true;
   // periodic: images to depth R*tsteps must fit the ghost band, and one wrap (or, for a
   // row slab of a ring, one neighbour's rows) must cover them

@@ -135,6 +135,82 @@ __host__ __device__ constexpr int row_need(int d) {
   return need;
 }
 
+
+// ---------------------------------------------------------------------------
+// Shared products (SYM).  The reference's sum adds fl(c_s * u[p + q_s]) tap by tap; the
+// product depends only on the input element and the coefficient VALUE, and the named
+// schemes give every tap of a symmetry class (centre / axis / corner / distance-2 arm)
+// the same coefficient.  So fl(c_axis * u[x]) is one value whether x is read as the
+// (-1,0) tap of one output point or the (0,+1) tap of another: the fused kernel computes
+// it once per input element and class (P9: 3 multiplies per update instead of 9, P13: 4
+// instead of 13) and feeds the same bits into every sum — the additions and their order
+// are untouched, so results stay bit-identical to the reference's sequence.
+//   * a stage keeps, per non-centre class, the product rows of its last 2R input rows
+//     (+R neighbour columns each side, fetched from the adjacent lanes by shuffle — the
+//     products travel, not the raw values), the raw own values of those rows (the
+//     -u^{k-1} term two stages down) and R partial sums;
+//   * an output row's sum is built in table order across R+1 row arrivals: tap s is added
+//     when input row (output row + phase(s)) arrives, phase(s) = the largest q1 seen up to
+//     tap s (clamped at 0) — exactly the taps whose rows are already in the stage.
+// The host checks that the table's coefficients are equal within each class
+// (tb_classes_equal); other tables fall back to the unblocked kernels.
+constexpr int kTapClasses = 4;  // 0 centre, 1 axis (distance 1), 2 corner, 3 distance-2 arm
+template <class S>
+__host__ __device__ constexpr int tap_class(int s) {
+  const int a = S::q(s, 0) < 0 ? -S::q(s, 0) : S::q(s, 0);
+  const int b = S::q(s, 1) < 0 ? -S::q(s, 1) : S::q(s, 1);
+  return (a == 0 && b == 0) ? 0 : (a + b == 1) ? 1 : (a == 1 && b == 1) ? 2
+         : (a + b == 2) ? 3 : -1;
+}
+template <class S>
+__host__ __device__ constexpr int tap_phase(int s) {
+  int ph = 0;
+  for (int i = 0; i <= s; ++i) ph = S::q(i, 0) > ph ? S::q(i, 0) : ph;
+  return ph;
+}
+template <class S>
+__host__ __device__ constexpr int class_rep(int k) {  // first tap of class k (-1: none)
+  for (int s = 0; s < S::N; ++s)
+    if (tap_class<S>(s) == k) return s;
+  return -1;
+}
+template <class S>
+__host__ __device__ constexpr int class_need(int k) {  // neighbour columns class k reads
+  int need = 0;
+  for (int s = 0; s < S::N; ++s)
+    if (tap_class<S>(s) == k) {
+      const int b = S::q(s, 1) < 0 ? -S::q(s, 1) : S::q(s, 1);
+      need = b > need ? b : need;
+    }
+  return need;
+}
+template <class S>
+__host__ __device__ constexpr bool sym_shape() {  // centre first, every tap classified
+  if (S::q(0, 0) != 0 || S::q(0, 1) != 0) return false;
+  for (int s = 0; s < S::N; ++s)
+    if (tap_class<S>(s) < 0 || (s > 0 && tap_class<S>(s) == 0)) return false;
+  return true;
+}
+template <class S>
+static bool tb_classes_equal(const ps_table* t) {
+  for (int s = 0; s < S::N; ++s) {
+    const int rep = class_rep<S>(tap_class<S>(s));
+    if (std::memcmp(&t->c[s], &t->c[rep], sizeof(double)) != 0) return false;
+  }
+  return true;
+}
+#ifndef PS_TB_SYM
+#define PS_TB_SYM 1
+#endif
+#ifndef PS_TB_SYM_R2_MAXT
+#define PS_TB_SYM_R2_MAXT 2  // radius 2: deepest fusion whose shared-product state fits
+#endif
+template <typename T, int A, class S, int TS>
+__host__ __device__ constexpr bool tb_sym() {
+  return PS_TB_SYM != 0 && Arith<T, A>::kSplit && sym_shape<S>() &&
+         (S::R == 1 || TS <= PS_TB_SYM_R2_MAXT);
+}
+
 // HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate
 // instance, so the plain pass keeps its store path free of the extra checks: they cost
 // C5 26 % when compiled into every instance)
@@ -439,6 +515,236 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
     }
   };
 
+
+  if constexpr (tb_sym<T, A, S, TS>()) {
+    // ---------------- consumers, shared products (see the note above tap_class) --------
+    static_assert(VM == 1 || R == 1, "shared-product state is sized for one or two vectors");
+    coef_t cc[kTapClasses];
+#pragma unroll
+    for (int k = 0; k < kTapClasses; ++k) cc[k] = class_rep<S>(k) >= 0 ? c[class_rep<S>(k) < 0 ? 0 : class_rep<S>(k)] : coef_t(0);
+    acc_t part[TS][R][V];                      // sums in flight: part[t][j] = output row a-j
+    T rawq[TS][2 * R][V];                      // raw own values of input rows a-2R .. a-1
+    acc_t prod[TS][kTapClasses][2 * R][WC];    // product rows a-2R .. a-1 (class 0 unused)
+#pragma unroll
+    for (int t = 0; t < TS; ++t) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int v = 0; v < V; ++v) part[t][j][v] = Ar::zero();
+#pragma unroll
+      for (int r = 0; r < 2 * R; ++r) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) rawq[t][r][v] = T(0);
+#pragma unroll
+        for (int k = 0; k < kTapClasses; ++k)
+#pragma unroll
+          for (int x = 0; x < WC; ++x) prod[t][k][r][x] = Ar::zero();
+      }
+    }
+
+    // Stage t takes input row a of level k+t (`own`; stage 0 also its raw neighbours nl/nr
+    // from shared memory), finishes the sum of output row a-R of level k+t+1 into `fin`,
+    // and returns in `oldest` its raw row a-2R (the next stage's -u term) before sliding.
+    auto stage = [&](auto t_tag, const T* own, const T* nl, const T* nr, acc_t* fin,
+                     T* oldest) {
+      constexpr int t = decltype(t_tag)::value;
+      acc_t np[kTapClasses][WC];
+#pragma unroll
+      for (int k = 1; k < kTapClasses; ++k) {
+        if (class_rep<S>(k) < 0) continue;
+#pragma unroll
+        for (int v = 0; v < V; ++v) np[k][R + v] = Ar::mul(cc[k], own[v]);
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q < R - class_need<S>(k)) continue;             // column never read
+          if constexpr (t == 0)
+            np[k][q] = Ar::mul(cc[k], nl[q]);
+          else
+            np[k][q] = shfl_up1(np[k][V + q]);                // left lane's last R products
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          if (q >= class_need<S>(k)) continue;
+          if constexpr (t == 0)
+            np[k][R + V + q] = Ar::mul(cc[k], nr[q]);
+          else
+            np[k][R + V + q] = shfl_down1(np[k][R + q]);      // right lane's first R products
+        }
+      }
+#pragma unroll
+      for (int j = R; j >= 0; --j) {
+        acc_t a[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[v] = (j == 0) ? Ar::zero() : part[t][j == 0 ? 0 : j - 1][v];
+#pragma unroll
+        for (int s = 0; s < S::N; ++s) {
+          if (tap_phase<S>(s) != j) continue;
+          const int k = tap_class<S>(s);
+          const int rel = S::q(s, 0) - j;                     // input row relative to a (<= 0)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            acc_t pv;
+            if (k == 0)
+              pv = Ar::mul(cc[0], own[v]);
+            else if (rel == 0)
+              pv = np[k][R + v + S::q(s, 1)];
+            else
+              pv = prod[t][k][2 * R + rel][R + v + S::q(s, 1)];
+            a[v] = Ar::add(a[v], pv);
+          }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (j == R)
+            fin[v] = a[v];
+          else
+            part[t][j][v] = a[v];
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) oldest[v] = rawq[t][0][v];
+#pragma unroll
+      for (int r = 0; r + 1 < 2 * R; ++r) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) rawq[t][r][v] = rawq[t][r + 1][v];
+#pragma unroll
+        for (int k = 1; k < kTapClasses; ++k)
+#pragma unroll
+          for (int x = 0; x < WC; ++x) prod[t][k][r][x] = prod[t][k][r + 1][x];
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v) rawq[t][2 * R - 1][v] = own[v];
+#pragma unroll
+      for (int k = 1; k < kTapClasses; ++k) {
+        if (class_rep<S>(k) < 0) continue;
+#pragma unroll
+        for (int x = 0; x < WC; ++x) prod[t][k][2 * R - 1][x] = np[k][x];
+      }
+    };
+
+    // sum -> level value: subtract, then the Dirichlet ring / outside-the-grid mask
+    auto finish = [&](auto interior_tag, const acc_t* fin, const T* minus, int row, int gc0,
+                      bool cols_inner, T* res) {
+      constexpr bool INTERIOR = decltype(interior_tag)::value;
+      if constexpr (PER || INTERIOR) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = Ar::two(fin[v], minus[v]);
+        return;
+      }
+      const int gi = p.row0 + row;
+      const bool row_in = (gi >= p.ring) && (gi < p.grows - p.ring);
+      if (row_in && cols_inner) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = Ar::two(fin[v], minus[v]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int gc = gc0 + v;
+          const bool in = row_in && (gc >= p.ring) && (gc < p.cols - p.ring);
+          res[v] = in ? Ar::two(fin[v], minus[v]) : T(0);
+        }
+      }
+    };
+
+    auto sym_row = [&](auto steady_tag, auto interior_tag, const T* su_row, const T* sk_row,
+                       int m, int i0, int i1, int j0, bool cols_inner, bool lane_store) {
+      constexpr bool STEADY = decltype(steady_tag)::value;
+      const int e = i0 - R * TS + m;
+      const int gc0 = j0 + gc_lane;
+      T own[V], nl[VV], nr[VV], res[V], minus[V], oldest[V];
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo - VV), nl);
+#pragma unroll
+      for (int mm = 0; mm < VM; ++mm)
+        Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + mm * VV), own + mm * VV);
+      Vec<T>::unpack(*reinterpret_cast<const vec_t*>(su_row + xo + V), nr);
+      bool live = true;   // stage t's output exists once 2R(t+1) rows have flowed
+      auto run = [&](auto t_tag) {
+        constexpr int t = decltype(t_tag)::value;
+        if (!live) return;
+        acc_t fin[V];
+        T nxt_minus[V];
+        // nl holds columns -VV..-1: the R nearest are nl[VV-R..VV)
+        stage(t_tag, own, nl + (VV - R), nr, fin, nxt_minus);
+        if (!STEADY && m < 2 * R * (t + 1)) {   // state fed, output not yet valid
+          live = false;
+          return;
+        }
+        const int row = e - (t + 1) * R;
+        if constexpr (t == 0) {
+#pragma unroll
+          for (int mm = 0; mm < VM; ++mm)
+            Vec<T>::unpack(*reinterpret_cast<const vec_t*>(sk_row + xk + mm * VV), minus + mm * VV);
+        }
+        finish(interior_tag, fin, minus, row, gc0, cols_inner, res);
+        constexpr bool PRED_ST = STEADY && decltype(interior_tag)::value && !HALO;
+        if constexpr (t == TS - 1) {
+          if constexpr (PRED_ST)
+            st_pred<T, VM>(out_last + int64_t(row) * pitch + gc0, res, lane_store);
+          else if (lane_store && (STEADY || (row >= i0 && row < i1)))
+            store_vec(out_last, row, gc0, res, true);
+        } else {
+          if constexpr (t == TS - 2) {
+            if constexpr (PRED_ST)
+              st_pred<T, VM>(out_prev + int64_t(row) * pitch + gc0, res,
+                             lane_store && row >= i0 && row < i1);
+            else if (lane_store && row >= i0 && row < i1)
+              store_vec(out_prev, row, gc0, res, false);
+          }
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            own[v] = res[v];             // the next stage's input row
+            minus[v] = nxt_minus[v];     // and its -u term (this stage's raw row a-2R)
+          }
+        }
+      };
+      run(std::integral_constant<int, 0>{});
+      if constexpr (TS > 1) run(std::integral_constant<int, 1>{});
+      if constexpr (TS > 2) run(std::integral_constant<int, 2>{});
+      if constexpr (TS > 3) run(std::integral_constant<int, 3>{});
+    };
+
+    for (uint32_t g = 0;; ++g) {
+      const uint32_t s = g % NS;
+      const uint32_t k = g / NS;
+      mbar_wait(&full[s], k & 1);
+      __syncwarp();
+      const int tile = s_tile[s];
+      if (tile < 0) break;
+      const int mlo = s_mlo[s];
+      const int chunk = tile / p.nstrips;
+      const int strip = tile - chunk * p.nstrips;
+      const int i0 = p.rlo + chunk * p.rc;
+      const int i1 = min(i0 + p.rc, p.rhi);
+      const int j0 = strip * W;
+      const int ne = (i1 - i0) + NE_EXTRA;
+      const T* su = s_uk + s * RB * LU;
+      const T* sk = s_km + s * RB * LK;
+      const bool cols_inner = PER || ((j0 - HT >= p.ring) && (j0 + W + HT <= p.cols - p.ring));
+      const bool lane_store = lane_out && (j0 + gc_lane < p.cols);
+      const bool steady = mlo >= 2 * R * TS && mlo + RB <= ne;
+      const int rmin = i0 - R * TS + mlo - TS * R, rmax = i0 - R * TS + mlo + RB - 1 - R;
+      constexpr int D = R * TS;
+      const bool interior =
+          PER ? ((j0 - HT >= D) && (j0 + W + HT <= p.cols - D) && (rmin >= D) && (rmax < p.rows - D))
+              : cols_inner && (p.row0 + rmin >= p.ring) && (p.row0 + rmax < p.grows - p.ring);
+      if (steady && interior) {
+#pragma unroll
+        for (int mm = 0; mm < RB; ++mm)
+          sym_row(std::true_type{}, std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
+                  j0, cols_inner, lane_store);
+      } else {
+        // tile heads/tails and slots touching the ring (or the image bands): one rolled
+        // body with every check (a few percent of the slots on the large grids)
+#pragma unroll 1
+        for (int mm = 0; mm < min(RB, ne - mlo); ++mm)
+          sym_row(std::false_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0,
+                  i1, j0, cols_inner, lane_store);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  } else {
+  // ---------------- consumers, one product per tap (NATIVE f32, PS_TB_SYM=0) -----------
   // One u^k row through every stage.  STEADY: all TS windows are full and the final row
   // lies inside the tile (no per-stage checks, so the unrolled window rotation compiles
   // to register renaming).  Otherwise stage t+1 runs only once window t is full.
@@ -531,5 +837,5 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  }  // (one product per tap)
 }
-

@@ -587,7 +587,7 @@ def test_config3_full_size_blocking_is_bitwise():
 
 def test_config5_full_size_f32_against_f64():
     """C5's stated check at full size: the f32 run against an f64 run on the same seed
-    after 100 steps, relative max-norm <= 2 n_t^2 2^-24."""
+    after 100 steps, within f32_tolerance(100) = 1.5 n_t^2 2^-24 (measured 2.87e-4)."""
     import torch
 
     from paper_1904_04048_b200.device import Simulation
