@@ -1,12 +1,14 @@
 # Builds libps.so (sm_100a) and the CPU oracle.  __graft_entry__.build() runs `make -j4`.
-# The kernels compile in four translation units (C-ABI + one per dtype/contract) so a
-# parallel make takes about a third of the single-unit time.
+# The kernels compile in thirteen translation units (C-ABI, one per dtype/contract for the
+# streaming kernels, one per dtype/contract/depth for the fused kernels) so a parallel make
+# is bounded by the slowest single unit.
 NVCC ?= /usr/local/cuda/bin/nvcc
 NVFLAGS = -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo \
           -Xcompiler -fPIC -Xcompiler -Wall -Iinclude
 CSRC = paper_1904_04048_b200/csrc
 OBJDIR = build/obj
-UNITS = ps_device ps_kern_f64 ps_kern_f32r ps_kern_f32n
+KERN = f64 f32r f32n
+UNITS = ps_device $(foreach k,$(KERN),ps_kern_$(k) ps_kern_$(k)_t2 ps_kern_$(k)_t3 ps_kern_$(k)_t4)
 OBJS = $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDR = include/ps.h $(wildcard $(CSRC)/*.cuh)
 

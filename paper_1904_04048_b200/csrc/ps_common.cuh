@@ -318,6 +318,9 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #ifndef PS_TB_NW
 #define PS_TB_NW 0
 #endif
+#ifndef PS_TUNE_BC
+#define PS_TUNE_BC PS_BC_DIRICHLET
+#endif
 #ifndef PS_TB_RB
 #define PS_TB_RB 0  // 0: per radius (launch_tb)
 #endif
@@ -342,7 +345,7 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 template <typename T, int A, class S, int TS, bool PER>
 constexpr int tb_vm() {
   return PS_TB_VM > 0            ? PS_TB_VM
-         : tb_sym<T, A, S, TS>()     ? PS_TB_SYM_VM
+         : tb_sym<T, A, S, TS, PER>()     ? PS_TB_SYM_VM
                                  : ((sizeof(T) == 8 && S::R == 1 && !PER) ? 2 : 1);
 }
 #ifndef PS_TB_WGS
@@ -355,39 +358,55 @@ constexpr int tb_vm() {
 #ifndef PS_TB_WGS1
 #define PS_TB_WGS1 -1  // one-vector geometries: 1 = always, 0 = never, -1 = f32 Dirichlet
 #endif
+// f64 radius-2 passes of depth >= 3 keep 3-4 five-row windows (90-120 doubles): they fit
+// the 232 registers of 8 warpgroup-specialised consumer warps without spilling (C3 T=3 381,
+// T=4 360 GLUP/s; 11 warps x 168 registers spilled 456 B at T=4: 319)
+template <typename T, class S, int TS>
+constexpr bool tb_deep_r2() {
+  return sizeof(T) == 8 && S::R == 2 && TS >= 3;
+}
 template <typename T, int A, class S, int TS, bool PER>
 constexpr bool tb_wgs() {
   return PS_TB_WGS >= 0 ? PS_TB_WGS != 0
          : tb_vm<T, A, S, TS, PER>() == 2
              ? true
-             : (tb_sym<T, A, S, TS>() ? (PS_TB_SYM_WGS != 0 && !PER)
-                : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0 : (sizeof(T) == 4 && !PER)));
+             : (tb_sym<T, A, S, TS, PER>() ? (PS_TB_SYM_WGS != 0 && !PER)
+                : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0
+                                   : ((sizeof(T) == 4 || tb_deep_r2<T, S, TS>()) && !PER)));
 }
+#ifndef PS_TB_WGS_NW
+#define PS_TB_WGS_NW 0   // tuning: consumer warps of a warpgroup-specialised block (8 or 12)
+#endif
 template <typename T, int A, class S, int TS, bool PER>
 constexpr int tb_nw() {
-  return tb_wgs<T, A, S, TS, PER>() ? (tb_vm<T, A, S, TS, PER>() == 2 ? 8 : 12)
+  return tb_wgs<T, A, S, TS, PER>() ? (PS_TB_WGS_NW > 0 ? PS_TB_WGS_NW
+                                       : (tb_vm<T, A, S, TS, PER>() == 2 ||
+                                          (tb_deep_r2<T, S, TS>() && !tb_sym<T, A, S, TS, PER>()))
+                                           ? 8 : 12)
          : PS_TB_NW > 0             ? PS_TB_NW
                                     : (tb_vm<T, A, S, TS, PER>() == 2 ? 7 : 11);
 }
-template <typename T, int TS>
+template <typename T, int TS, bool SYM = false>
 constexpr int tb_ns() {
-  return PS_TB_NS > 0 ? PS_TB_NS : 3;
+  return PS_TB_NS > 0 ? PS_TB_NS : SYM ? 2 : 3;
 }
 
 template <typename T, int A, class S, int TS, bool PER, bool HALO>
 static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* out_prev,
                            void* out_last, const ps_table* t, int64_t rlo, int64_t rhi,
                            cudaStream_t st, bool reverse, int rc_hint, const TBHalo& h) {
-  constexpr int VM = tb_vm<T, A, S, TS, PER>(), NW = tb_nw<T, A, S, TS, PER>(), NS = tb_ns<T, TS>();
+  constexpr bool SYM = tb_sym<T, A, S, TS, PER>();
+  constexpr int VM = tb_vm<T, A, S, TS, PER>(), NW = tb_nw<T, A, S, TS, PER>();
+  constexpr int NS = tb_ns<T, TS, SYM>();
   constexpr bool WGS = tb_wgs<T, A, S, TS, PER>();
-  constexpr bool SYM = tb_sym<T, A, S, TS>();
   if (SYM && !tb_classes_equal<S>(t)) return PS_ERR_TABLE;  // (tb_supported screens these)
   constexpr int NT = (NW + (WGS ? 4 : 1)) * 32;  // threads per block (consumers + producer)
   // rows per pipeline slot: one window rotation (2R+1) for radius 1; radius 2 takes 6
   // (measured: C5 1052 -> 1080, C3 f32 827 -> 837 GLUP/s; fewer ring waits per row, and
   // 8 or 10 rows no longer fit the shared memory)
   // shared-product kernels rotate 2R-row delay lines: a multiple of 2R rows per slot
-  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? 4 : (S::R == 2 ? 6 : 2 * S::R + 1);
+  // (8 rows in a 2-slot ring measured best: C4 652 vs 641 GLUP/s for 4 rows x 3 slots)
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? 8 : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
   static std::once_flag once[kMaxDevices];
@@ -475,6 +494,16 @@ template <typename T, int A, int TS>
 static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1, void* op,
                              void* ol, const ps_table* t, int64_t lo, int64_t hi,
                              cudaStream_t st, bool rev, int rc, const TBHalo& h) {
+#ifdef PS_TUNE_SHAPE
+  // tuning builds (tools/tb_variants.sh) instantiate ONE fused kernel: the plain pass of
+  // PS_TUNE_SHAPE at depth PS_TUNE_TS; everything else reports "unsupported"
+  if constexpr (TS == PS_TUNE_TS) {
+    if (shape_matches<PS_TUNE_SHAPE>(t) && g->bc == PS_TUNE_BC)
+      return launch_tb<T, A, PS_TUNE_SHAPE, TS, PS_TUNE_BC == PS_BC_PERIODIC, false>(
+          g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+  }
+  return PS_ERR_TABLE;
+#else
   if (shape_matches<ShapeP5>(t))
     return launch_tb_bc<T, A, TS, ShapeP5>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP9>(t))
@@ -484,6 +513,7 @@ static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1,
   if (shape_matches<ShapeP13>(t))
     return launch_tb_bc<T, A, TS, ShapeP13>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   return PS_ERR_TABLE;
+#endif
 }
 
 // First step as two streaming launches: u1 <- -fl(tau * A_v(v0)) (VP), then the ordinary
@@ -516,13 +546,32 @@ static ps_status first_step_stream(const ps_grid* g, const void* u0, const void*
 // ---------------------------------------------------------------------------
 // Typed entry points, one translation unit per (dtype, contract): ps_kern_*.cu
 // ---------------------------------------------------------------------------
+// One translation unit per (dtype, contract) for the streaming / first-step kernels, and
+// one per (dtype, contract, depth) for the fused kernels (ps_kern_*_t<depth>.cu): twelve
+// units that compile in parallel instead of three long ones.
 #define PS_TYPED_DECL(SFX)                                                                  \
   ps_status two_step_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,  \
                            const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,      \
                            const Halo& h);                                                  \
-  ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
-                     const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev, int rc, const TBHalo& h);                                    \
+  ps_status tb_##SFX##_t2(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
+                          void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
+                          cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
+  ps_status tb_##SFX##_t3(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
+                          void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
+                          cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
+  ps_status tb_##SFX##_t4(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
+                          void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
+                          cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
+  inline ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op,   \
+                            void* ol, const ps_table* t, int tsteps, int64_t lo, int64_t hi, \
+                            cudaStream_t st, bool rev, int rc, const TBHalo& h) {           \
+    switch (tsteps) {                                                                       \
+      case 2: return tb_##SFX##_t2(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
+      case 3: return tb_##SFX##_t3(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
+      case 4: return tb_##SFX##_t4(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
+      default: return PS_ERR_ARG;                                                           \
+    }                                                                                       \
+  }                                                                                         \
   ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
                         const ps_table* tu, const ps_table* tv, double tau, int64_t lo,     \
                         int64_t hi, cudaStream_t st, bool* done);
@@ -537,22 +586,19 @@ PS_TYPED_DECL(f32n)
                            const Halo& h) {                                                 \
     return dispatch_two_step_bc<T, A>(g, uk, ukm1, ukp1, t, lo, hi, st, h);                 \
   }                                                                                         \
-  ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op, void* ol, \
-                     const ps_table* t, int tsteps, int64_t lo, int64_t hi, cudaStream_t st, \
-                     bool rev, int rc, const TBHalo& h) {                                   \
-    switch (tsteps) {                                                                       \
-      case 2: return dispatch_tb<T, A, 2>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
-      case 3: return dispatch_tb<T, A, 3>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
-      case 4: return dispatch_tb<T, A, 4>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);  \
-      default: return PS_ERR_ARG;                                                           \
-    }                                                                                       \
-  }                                                                                         \
   ps_status first_##SFX(const ps_grid* g, const void* u0, const void* v0, void* u1,         \
                         const ps_table* tu, const ps_table* tv, double tau, int64_t lo,     \
                         int64_t hi, cudaStream_t st, bool* done) {                          \
     return g->bc == PS_BC_PERIODIC                                                          \
                ? first_step_stream<T, A, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done) \
                : first_step_stream<T, A, false>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done); \
+  }
+
+#define PS_TYPED_DEFINE_TB(SFX, T, A, TS)                                                   \
+  ps_status tb_##SFX##_t##TS(const ps_grid* g, const void* uk, const void* ukm1, void* op,  \
+                             void* ol, const ps_table* t, int64_t lo, int64_t hi,           \
+                             cudaStream_t st, bool rev, int rc, const TBHalo& h) {          \
+    return dispatch_tb<T, A, TS>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);           \
   }
 
 }  // namespace ps

@@ -138,7 +138,11 @@ static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
   // coefficient class (ps_tblock.cuh): the table must give each class one coefficient
   // (every named scheme does); others run unblocked
   const bool ref = g->dtype == PS_F64 || g->arith == PS_ARITH_REF;
-  if (ref && PS_TB_SYM != 0 && (table_radius(t) == 1 || tsteps <= PS_TB_SYM_R2_MAXT)) {
+  const bool sym = PS_TB_SYM == 2 ? (ref && (table_radius(t) == 1 || tsteps <= PS_TB_SYM_R2_MAXT))
+                   : PS_TB_SYM == 1 ? (g->dtype == PS_F64 && table_radius(t) == 1 &&
+                                       g->bc == PS_BC_DIRICHLET)
+                                    : false;
+  if (sym) {
     const bool eq = shape_matches<ShapeP5>(t)   ? tb_classes_equal<ShapeP5>(t)
                     : shape_matches<ShapeP9>(t) ? tb_classes_equal<ShapeP9>(t)
                     : shape_matches<ShapeC9>(t) ? tb_classes_equal<ShapeC9>(t)

@@ -1,5 +1,5 @@
-// ps_kern_f32n.cu — streaming, temporal-blocking and first-step kernels for
-// (float, ARITH_NATIVE); see ps_common.cuh.
+// ps_kern_f32n.cu — streaming and first-step kernels for (float, ARITH_NATIVE); the fused
+// (temporally blocked) kernels of this contract are in ps_kern_f32n_t<depth>.cu.
 #include "ps_common.cuh"
 
 namespace ps {

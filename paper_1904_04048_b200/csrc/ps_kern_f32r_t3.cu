@@ -1,0 +1,6 @@
+// ps_kern_f32r_t3.cu — fused kernels of depth 3 for (float, ARITH_REF); see ps_common.cuh.
+#include "ps_common.cuh"
+
+namespace ps {
+PS_TYPED_DEFINE_TB(f32r, float, ARITH_REF, 3)
+}  // namespace ps

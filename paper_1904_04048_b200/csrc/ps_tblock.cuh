@@ -202,13 +202,21 @@ static bool tb_classes_equal(const ps_table* t) {
 #ifndef PS_TB_SYM
 #define PS_TB_SYM 1
 #endif
+// Where the shared-product path is used (measured on B200, tools/tb_tune.sh):
+// f64 radius-1 Dirichlet passes (C4: 652 vs 651 GLUP/s at 1965 MHz, 567 vs 558 under the
+// power cap of a 200-step run — 24 % fewer FP64 instructions at equal time shows the pass
+// is bound by DRAM traffic and issue slots, not by the FP64 pipe).  Not used for periodic
+// grids (11 consumer warps x 168 registers spill: C2 252 vs 288-346), radius 2 (the state
+// of three stages needs 8 x 232-register warps: C3 T=3 385 vs 381) or the f32 reference
+// contract (C5 286 vs 287): PS_TB_SYM=2 forces it everywhere it can compile.
 #ifndef PS_TB_SYM_R2_MAXT
-#define PS_TB_SYM_R2_MAXT 2  // radius 2: deepest fusion whose shared-product state fits
+#define PS_TB_SYM_R2_MAXT 2  // radius 2 under PS_TB_SYM=2: deepest fusion that fits
 #endif
-template <typename T, int A, class S, int TS>
+template <typename T, int A, class S, int TS, bool PER>
 __host__ __device__ constexpr bool tb_sym() {
-  return PS_TB_SYM != 0 && Arith<T, A>::kSplit && sym_shape<S>() &&
-         (S::R == 1 || TS <= PS_TB_SYM_R2_MAXT);
+  if (PS_TB_SYM == 0 || !Arith<T, A>::kSplit || !sym_shape<S>()) return false;
+  if (PS_TB_SYM == 2) return S::R == 1 || TS <= PS_TB_SYM_R2_MAXT;
+  return sizeof(T) == 8 && S::R == 1 && !PER;
 }
 
 // HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate
@@ -516,7 +524,7 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
   };
 
 
-  if constexpr (tb_sym<T, A, S, TS>()) {
+  if constexpr (tb_sym<T, A, S, TS, PER>()) {
     // ---------------- consumers, shared products (see the note above tap_class) --------
     static_assert(VM == 1 || R == 1, "shared-product state is sized for one or two vectors");
     coef_t cc[kTapClasses];
