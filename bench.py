@@ -40,7 +40,7 @@ CONFIGS = {
                steps=1000, ic="standing", tb=4,
                desc="C2: P9 9-point, 4096^2 f64 periodic, lambda=0.6, standing wave m=4 n=6, 1000 steps"),
     "C3": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f64", arith="ref", lam=0.4,
-               steps=500, ic=(32, 0.01, 0.05, False), tb=2,
+               steps=500, ic=(32, 0.01, 0.05, False), tb=3,
                desc="C3: P13 13-point, 16384^2 f64, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C3f32": dict(scheme="P13", n=16383, bc="dirichlet", ring=2, dtype="f32", arith="native",
                   lam=0.4, steps=500, ic=(32, 0.01, 0.05, False), tb=4,
@@ -885,7 +885,7 @@ def main():
                          "3 while a region takes under 2 s, else 1")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 3, 4),
                     help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
-                         "C3 f32: 4, C3 f64: 2, with an unblocked companion measurement; C1: 1)")
+                         "C3 f32: 4, C3 f64: 3, with an unblocked companion measurement; C1: 1)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.arith and cfg["dtype"] == "f32":
