@@ -365,6 +365,9 @@ class DistributedSlabs:
         self._graphs = {}
         self._seen = set()
         self.graphed = False     # True once a pass has been replayed from a CUDA graph
+        # kernels executed through graph replays minus those merely recorded at capture:
+        # add to libps.so's ps_launch_count() delta for the launches that actually ran
+        self.launch_correction = 0
         self.graph_error = None
         self._err = None
         if transport == "p2p":
@@ -597,8 +600,13 @@ class DistributedSlabs:
             try:
                 torch.cuda.synchronize()
                 g = torch.cuda.CUDAGraph()
+                before = nat.launch_count()
                 with torch.cuda.graph(g):
                     body()
+                # launches recorded into the graph were counted by libps.so as issued; they
+                # run once per replay instead
+                g.kernels = nat.launch_count() - before
+                self.launch_correction -= g.kernels
                 self._graphs[key] = g
             except Exception as exc:  # capture is an optimisation, never a requirement
                 self.graph_error = f"{type(exc).__name__}: {exc}"
@@ -608,6 +616,7 @@ class DistributedSlabs:
                 return False
             # capture records, it does not execute: replay below runs the pass
         g.replay()
+        self.launch_correction += g.kernels
         self.graphed = True
         return True
 
