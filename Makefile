@@ -8,7 +8,8 @@ NVFLAGS = -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo \
 CSRC = paper_1904_04048_b200/csrc
 OBJDIR = build/obj
 KERN = f64 f32r f32n
-UNITS = ps_device $(foreach k,$(KERN),ps_kern_$(k) ps_kern_$(k)_t2 ps_kern_$(k)_t3 ps_kern_$(k)_t4)
+UNITS = ps_device $(foreach k,$(KERN),ps_kern_$(k) ps_kern_$(k)_t2 ps_kern_$(k)_t3 ps_kern_$(k)_t4) \
+        ps_kern_f64_t5 ps_kern_f64_t6
 OBJS = $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDR = include/ps.h $(wildcard $(CSRC)/*.cuh)
 

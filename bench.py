@@ -46,7 +46,7 @@ CONFIGS = {
                   lam=0.4, steps=500, ic=(32, 0.01, 0.05, False), tb=4,
                   desc="C3: P13 13-point, 16384^2 f32, Dirichlet ring 2, lambda=0.4, 500 steps"),
     "C4": dict(scheme="P9", n=32767, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.6,
-               steps=200, ic=(64, 0.01, 0.05, True), tb=4,
+               steps=200, ic=(64, 0.01, 0.05, True), tb=5,
                desc="C4: P9 9-point, 32768^2 f64, Dirichlet ring 1, lambda=0.6, 200 steps"),
     "C5": dict(scheme="P13", n=65535, bc="dirichlet", ring=2, dtype="f32", arith="native",
                lam=0.4, steps=100, ic=(128, 0.002, 0.01, False), tb=4,
@@ -883,9 +883,10 @@ def main():
     ap.add_argument("--reps", type=int, default=0,
                     help="repetitions of the K-step timed region (median reported); 0 = auto: "
                          "3 while a region takes under 2 s, else 1")
-    ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 3, 4),
-                    help="temporal blocking depth; 0 = the config's measured best (C2/C4/C5 and "
-                         "C3 f32: 4, C3 f64: 3, with an unblocked companion measurement; C1: 1)")
+    ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 3, 4, 5, 6),
+                    help="temporal blocking depth; 0 = the config's measured best (C4: 5; C2, C5 "
+                         "and C3 f32: 4; C3 f64: 3; with an unblocked companion measurement; "
+                         "C1: 1)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.arith and cfg["dtype"] == "f32":

@@ -170,7 +170,7 @@ ps_status ps_ipc_close(void* dev_ptr);
 ps_status ps_march(const ps_grid* g, void* lvl[3], int64_t nsteps, const ps_table* t,
                    int32_t* newest, void* stream);
 
-/* Temporal blocking: tsteps (2, 3 or 4) two-step updates fused into one
+/* Temporal blocking: tsteps (2..4; 5 and 6 for f64 radius-1 Dirichlet tables) updates fused into one
  * streaming pass over u^k / u^{k-1}; writes only u^{k+tsteps-1} (out_prev) and
  * u^{k+tsteps} (out_last).  HBM traffic 4/tsteps words per update instead of 3.
  * Dirichlet grids, shapes P5/P9/C9/P13; results bitwise equal to tsteps ps_two_step
@@ -199,7 +199,7 @@ ps_status ps_two_step_tb_halo(const ps_grid* g, const void* uk, const void* ukm1
                               int64_t row_lo, int64_t row_hi, void* up_prev, void* up_last,
                               int64_t up_rows, void* dn_prev, void* dn_last, void* stream);
 
-/* nsteps updates over four rotating levels with temporal blocking depth tsteps (1..4);
+/* nsteps updates over four rotating levels with temporal blocking depth tsteps (1..6);
  * lvl[*newest] = u^k and lvl[*previous] = u^{k-1} on entry and on return.  nsteps not
  * divisible by tsteps finishes with single steps. */
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
@@ -225,7 +225,7 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
  * elements with row stride host_pitch, a = 1 for periodic grids (the reference's
  * alias row/column), 0 for Dirichlet; pinned memory for full copy bandwidth.
  * nsteps >= 1 = the time level returned (1 = the first step only).  tsteps: temporal
- * blocking depth (1..4; reduced to 1 for tables without a fused kernel).
+ * blocking depth (1..6; reduced to 1 for tables without a fused kernel at that depth).
  * nbands: 0 = auto (about 1024 rows per band).  Returns when the work is enqueued on
  * `stream`; out_host is valid after the stream synchronises. */
 typedef enum ps_solve_kind {

@@ -379,16 +379,18 @@ constexpr bool tb_wgs() {
 #endif
 template <typename T, int A, class S, int TS, bool PER>
 constexpr int tb_nw() {
+  // shared-product kernels: 8 consumer warps x 232 registers (no spills; 12 x 160 spill
+  // 80-116 B: C4 600 vs 568 GLUP/s on the 200-step run)
   return tb_wgs<T, A, S, TS, PER>() ? (PS_TB_WGS_NW > 0 ? PS_TB_WGS_NW
                                        : (tb_vm<T, A, S, TS, PER>() == 2 ||
-                                          (tb_deep_r2<T, S, TS>() && !tb_sym<T, A, S, TS, PER>()))
+                                          tb_deep_r2<T, S, TS>() || tb_sym<T, A, S, TS, PER>())
                                            ? 8 : 12)
          : PS_TB_NW > 0             ? PS_TB_NW
                                     : (tb_vm<T, A, S, TS, PER>() == 2 ? 7 : 11);
 }
 template <typename T, int TS, bool SYM = false>
 constexpr int tb_ns() {
-  return PS_TB_NS > 0 ? PS_TB_NS : SYM ? 2 : 3;
+  return PS_TB_NS > 0 ? PS_TB_NS : 3;
 }
 
 template <typename T, int A, class S, int TS, bool PER, bool HALO>
@@ -405,7 +407,7 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   // (measured: C5 1052 -> 1080, C3 f32 827 -> 837 GLUP/s; fewer ring waits per row, and
   // 8 or 10 rows no longer fit the shared memory)
   // shared-product kernels rotate 2R-row delay lines: a multiple of 2R rows per slot
-  // (8 rows in a 2-slot ring measured best: C4 652 vs 641 GLUP/s for 4 rows x 3 slots)
+  // (8 warps: 8 rows x 3 slots 664-692 GLUP/s on C4, 8 x 2 573-583, 4 x 3 603-606)
   constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? 8 : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
@@ -504,6 +506,26 @@ static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1,
   }
   return PS_ERR_TABLE;
 #else
+  if constexpr (TS >= 5) {
+    // deep fusion: shared-product kernels only (their 15-double stage state is what makes
+    // five or six stages fit 232 registers), Dirichlet, plain pass or in-kernel halo pass
+    if (g->bc != PS_BC_DIRICHLET) return PS_ERR_ARG;
+    const bool halo = h.up_prev || h.up_last || h.dn_prev || h.dn_last;
+    auto go = [&](auto shape) -> ps_status {
+      using S = decltype(shape);
+      if constexpr (tb_sym<T, A, S, TS, false>()) {
+        if (halo)
+          return launch_tb<T, A, S, TS, false, true>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+        return launch_tb<T, A, S, TS, false, false>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+      } else {
+        return PS_ERR_ARG;
+      }
+    };
+    if (shape_matches<ShapeP5>(t)) return go(ShapeP5{});
+    if (shape_matches<ShapeP9>(t)) return go(ShapeP9{});
+    if (shape_matches<ShapeC9>(t)) return go(ShapeC9{});
+    return PS_ERR_TABLE;
+  }
   if (shape_matches<ShapeP5>(t))
     return launch_tb_bc<T, A, TS, ShapeP5>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
   if (shape_matches<ShapeP9>(t))
@@ -562,6 +584,12 @@ static ps_status first_step_stream(const ps_grid* g, const void* u0, const void*
   ps_status tb_##SFX##_t4(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
                           void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
                           cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
+  ps_status tb_##SFX##_t5(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
+                          void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
+                          cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
+  ps_status tb_##SFX##_t6(const ps_grid* g, const void* uk, const void* ukm1, void* op,     \
+                          void* ol, const ps_table* t, int64_t lo, int64_t hi,              \
+                          cudaStream_t st, bool rev, int rc, const TBHalo& h);              \
   inline ps_status tb_##SFX(const ps_grid* g, const void* uk, const void* ukm1, void* op,   \
                             void* ol, const ps_table* t, int tsteps, int64_t lo, int64_t hi, \
                             cudaStream_t st, bool rev, int rc, const TBHalo& h) {           \
@@ -569,6 +597,8 @@ static ps_status first_step_stream(const ps_grid* g, const void* u0, const void*
       case 2: return tb_##SFX##_t2(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
       case 3: return tb_##SFX##_t3(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
       case 4: return tb_##SFX##_t4(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
+      case 5: return tb_##SFX##_t5(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
+      case 6: return tb_##SFX##_t6(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);         \
       default: return PS_ERR_ARG;                                                           \
     }                                                                                       \
   }                                                                                         \
@@ -592,6 +622,15 @@ PS_TYPED_DECL(f32n)
     return g->bc == PS_BC_PERIODIC                                                          \
                ? first_step_stream<T, A, true>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done) \
                : first_step_stream<T, A, false>(g, u0, v0, u1, tu, tv, tau, lo, hi, st, done); \
+  }
+
+// depths 5 and 6 exist for the shared-product kernels only (f64, radius 1, Dirichlet);
+// the other contracts define stubs
+#define PS_TYPED_DEFINE_TB_STUB(SFX, TS)                                                    \
+  ps_status tb_##SFX##_t##TS(const ps_grid*, const void*, const void*, void*, void*,        \
+                             const ps_table*, int64_t, int64_t, cudaStream_t, bool, int,    \
+                             const TBHalo&) {                                               \
+    return PS_ERR_ARG;                                                                      \
   }
 
 #define PS_TYPED_DEFINE_TB(SFX, T, A, TS)                                                   \

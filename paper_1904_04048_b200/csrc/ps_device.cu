@@ -134,6 +134,11 @@ static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
   const bool shape = shape_matches<ShapeP5>(t) || shape_matches<ShapeP9>(t) ||
                      shape_matches<ShapeC9>(t) || shape_matches<ShapeP13>(t);
   if (!shape || g->rows < 4 || g->cols < 4) return false;
+  if (tsteps < 2 || tsteps > 6) return false;
+  // depths 5 and 6: shared-product kernels only (f64, radius 1, Dirichlet)
+  if (tsteps >= 5 && (PS_TB_SYM == 0 || g->dtype != PS_F64 || table_radius(t) != 1 ||
+                      g->bc != PS_BC_DIRICHLET))
+    return false;
   // the reference-contract fused kernels share one product per input element and
   // coefficient class (ps_tblock.cuh): the table must give each class one coefficient
   // (every named scheme does); others run unblocked
@@ -591,7 +596,7 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
   for (int x = 0; x < 4; ++x)
     if (!lvl[x] || !aligned16(lvl[x])) return lvl[x] ? PS_ERR_ALIGN : PS_ERR_ARG;
   if ((s = check_table(g, t)) != PS_OK) return s;
-  if (tsteps < 1 || tsteps > 4) return PS_ERR_ARG;
+  if (tsteps < 1 || tsteps > 6) return PS_ERR_ARG;
   if (tsteps > 1 && !tb_supported(g, t, tsteps)) return PS_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int64_t k = 0;

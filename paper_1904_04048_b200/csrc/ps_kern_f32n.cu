@@ -4,4 +4,6 @@
 
 namespace ps {
 PS_TYPED_DEFINE(f32n, float, ARITH_NATIVE)
+PS_TYPED_DEFINE_TB_STUB(f32n, 5)
+PS_TYPED_DEFINE_TB_STUB(f32n, 6)
 }  // namespace ps

@@ -4,4 +4,6 @@
 
 namespace ps {
 PS_TYPED_DEFINE(f32r, float, ARITH_REF)
+PS_TYPED_DEFINE_TB_STUB(f32r, 5)
+PS_TYPED_DEFINE_TB_STUB(f32r, 6)
 }  // namespace ps

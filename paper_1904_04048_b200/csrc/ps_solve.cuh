@@ -48,7 +48,7 @@ static int64_t solve_auto_bands(int64_t rows, int s) {
 static ps_status build_solve_plan(const SolvePlanIn& in, std::vector<ps_solve_op>& ops) {
   ops.clear();
   if (in.rows < 1 || in.radius < 0 || in.nsteps < 1) return PS_ERR_ARG;
-  if (in.tsteps < 1 || in.tsteps > 4) return PS_ERR_ARG;
+  if (in.tsteps < 1 || in.tsteps > 6) return PS_ERR_ARG;
   if (in.nstreams < 1 || in.nstreams > 8 || in.nbands < 0) return PS_ERR_ARG;
   const int T = in.tsteps;
   const int64_t m = in.nsteps - 1;                    // two-step updates after the first step
@@ -196,7 +196,7 @@ ps_status ps_solve_host(const ps_grid* g, void* lvl[4], const void* u0_host,
   ps_status s = check_grid(g);
   if (s != PS_OK) return s;
   if (!lvl || !u0_host || !out_host || nsteps < 1 || nbands < 0) return PS_ERR_ARG;
-  if (tsteps < 1 || tsteps > 4) return PS_ERR_ARG;
+  if (tsteps < 1 || tsteps > 6) return PS_ERR_ARG;
   for (int x = 0; x < 4; ++x) {
     if (!lvl[x]) return PS_ERR_ARG;
     if (!aligned16(lvl[x])) return PS_ERR_ALIGN;
@@ -240,7 +240,11 @@ ps_status ps_solve_host(const ps_grid* g, void* lvl[4], const void* u0_host,
   in.nsteps = nsteps;
   in.tsteps = tsteps;
   in.nbands = env_int("PS_SOLVE_BANDS", nbands);
-  in.nstreams = std::max(1, std::min(8, env_int("PS_SOLVE_STREAMS", 2)));
+  // three compute streams: with the 672-column strips of the shared-product kernel a
+  // 1024-row band is 1.3 waves of tiles, and a third stream keeps the tail of one band's
+  // launch covered (C4, 200 steps: 395-400 ms for 16-48 bands; two streams 403-479 ms;
+  // profiles/r02_solve_tune_c4.jsonl)
+  in.nstreams = std::max(1, std::min(8, env_int("PS_SOLVE_STREAMS", 3)));
   std::vector<ps_solve_op> plan;
   if ((s = build_solve_plan(in, plan)) != PS_OK) return s;
   // fused passes in bands: taller tiles than the whole-grid heuristic picks for a short

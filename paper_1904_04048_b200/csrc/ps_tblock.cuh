@@ -709,6 +709,9 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
       if constexpr (TS > 1) run(std::integral_constant<int, 1>{});
       if constexpr (TS > 2) run(std::integral_constant<int, 2>{});
       if constexpr (TS > 3) run(std::integral_constant<int, 3>{});
+      if constexpr (TS > 4) run(std::integral_constant<int, 4>{});
+      if constexpr (TS > 5) run(std::integral_constant<int, 5>{});
+      static_assert(TS <= 6, "add a stage call per extra depth");
     };
 
     for (uint32_t g = 0;; ++g) {

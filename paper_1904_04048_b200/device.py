@@ -47,8 +47,8 @@ class Simulation:
         radius = self.spec.radius
         self.ring = (radius if ring is None else int(ring)) if bc == "dirichlet" else 0
         self.rows = self.n + 1 if bc == "dirichlet" else self.n
-        if tsteps not in (1, 2, 3, 4):
-            raise ValueError(f"tsteps must be 1, 2, 3 or 4, got {tsteps}")
+        if tsteps not in (1, 2, 3, 4, 5, 6):
+            raise ValueError(f"tsteps must be 1..6, got {tsteps}")
         self.tsteps = int(tsteps)
         # periodic blocked passes read wrap-around images R*T deep
         ghost = max(2, radius * tsteps) if bc == "periodic" else max(2, radius)

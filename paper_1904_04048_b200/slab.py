@@ -127,8 +127,8 @@ def rows_view(level: nat.Level, first: int, count: int):
 def _check_common(transport, transports, tsteps, bc):
     if transport not in transports:
         raise ValueError(f"transport must be one of {transports}, got {transport!r}")
-    if tsteps not in (1, 2, 3, 4):
-        raise ValueError(f"tsteps must be 1, 2, 3 or 4, got {tsteps}")
+    if tsteps not in (1, 2, 3, 4, 5, 6):
+        raise ValueError(f"tsteps must be 1..6, got {tsteps}")
     if bc not in ("dirichlet", "periodic"):
         raise ValueError(f"bc must be 'dirichlet' or 'periodic', got {bc!r}")
 

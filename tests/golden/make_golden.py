@@ -16,8 +16,9 @@ an alias straight from its source tree; nothing is copied.  Outputs (committed):
   runs.json     run() reports (error, per-step errors) for the paper tables
                 (benchmarks.py:27-61 rows) and a few extra configs.
 
-The GPU parity tests (tests/test_gpu_parity.py) and the oracle pin tests
-(tests/test_oracle_golden.py) read these files; neither touches /root/reference.
+The oracle pin tests (tests/test_host.py) and the GPU parity tests
+(tests/test_gpu_parity.py, tests/test_gpu_integration.py) read these files; none of
+them touches /root/reference.
 """
 
 from __future__ import annotations

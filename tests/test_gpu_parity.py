@@ -424,6 +424,43 @@ def test_temporal_blocking_bitwise_vs_oracle(name, radius, dtype, arith, tsteps,
     assert same_bits(sim.field("previous"), want_prev)
 
 
+@pytest.mark.parametrize("name", ["P5", "P9", "C9"])
+@pytest.mark.parametrize("tsteps", [5, 6])
+@pytest.mark.parametrize("n", [45, 700, 2100])
+def test_deep_blocking_f64_radius1_bitwise_vs_oracle(name, tsteps, n, oracle):
+    """Depths 5 and 6 (shared-product kernels: f64, radius 1, Dirichlet) equal T single
+    steps bit for bit, incl. a remainder and a second blocked call."""
+    from paper_1904_04048_b200.device import Simulation
+
+    sim = Simulation(name, n, 0.6, bc="dirichlet", tsteps=tsteps)
+    rng = np.random.default_rng(3 * n + tsteps)
+    u0, v0 = rng.normal(size=(n + 1, n + 1)), rng.normal(size=(n + 1, n + 1))
+    sim.load_initial(u0, v0)
+    sim.first_step()
+    steps = 2 * tsteps + 1
+    sim.march(steps)
+    sim.march(tsteps)
+    o1 = oracle.first_step(u0, v0, pairs(sim.spec, "first_u", 0.6), pairs(sim.spec, "first_v", 0.6),
+                           sim.tau, "dirichlet", 1)
+    want, want_prev = oracle.march(o1, u0, pairs(sim.spec, "two_step", 0.6), steps + tsteps,
+                                   "dirichlet", 1)
+    assert same_bits(sim.field(), want)
+    assert same_bits(sim.field("previous"), want_prev)
+
+
+def test_deep_blocking_is_refused_where_no_kernel_exists(nat):
+    """Depth 5/6 outside f64 radius-1 Dirichlet: the C-ABI says so (no silent fallback)."""
+    from paper_1904_04048_b200.device import Simulation
+
+    for kw in (dict(scheme="P13", bc="dirichlet"), dict(scheme="P9", bc="periodic"),
+               dict(scheme="P9", bc="dirichlet", dtype="f32", arith="native")):
+        sim = Simulation(kw.pop("scheme"), 300, 0.4, tsteps=5, **kw)
+        sim.gaussian_initial(4, 0.05, 0.1, seed=0)
+        sim.first_step()
+        with pytest.raises(nat.PsStatusError):
+            sim.march(5)
+
+
 def test_temporal_blocking_large_grid_matches_single_steps():
     """C5 shape (P13, ring 2, f32 native) on a 4096^2 grid: T=2 and T=4 marches equal the
     T=1 march bit for bit after 12 steps."""
@@ -567,8 +604,8 @@ def test_config4_full_size_blocking_is_bitwise():
     passes + 2 single steps) both live levels carry the T=1 march's bits."""
     args = ("P9", 32767, 0.6, "f64", "ref", (64, 0.01, 0.05, True))
     want = _full_size_checksums(*args, 1, 42)
-    assert _full_size_checksums(*args, 4, 42) == want
-    assert _full_size_checksums(*args, 2, 42) == want
+    for ts in (4, 5, 6, 2):
+        assert _full_size_checksums(*args, ts, 42) == want, ts
 
 
 def test_config3_full_size_blocking_is_bitwise():

@@ -193,6 +193,7 @@ def _spawn(world, *args):
     (2, "P13", "f64", "ref", 2, "dirichlet", "p2p"),
     (3, "P13", "f32", "native", 4, "dirichlet", "p2p"),
     (2, "P9", "f64", "ref", 4, "dirichlet", "nccl"),
+    (2, "P9", "f64", "ref", 5, "dirichlet", "p2p"),
     (3, "P13", "f64", "ref", 1, "periodic", "nccl"),
     (2, "P9", "f64", "ref", 2, "periodic", "nccl"),
 ])

@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 CASES = {
     # name: (scheme, n, lam, dtype, arith, (K, wmin, wmax, v_zero), steps, tsteps)
-    "C4": ("P9", 32767, 0.6, "f64", "ref", (64, 0.01, 0.05, True), 200, 4),
+    "C4": ("P9", 32767, 0.6, "f64", "ref", (64, 0.01, 0.05, True), 200, None),
     "C3": ("P13", 16383, 0.4, "f64", "ref", (32, 0.01, 0.05, False), 500, None),
     "C3f32ref": ("P13", 16383, 0.4, "f32", "ref", (32, 0.01, 0.05, False), 500, 2),
 }

@@ -58,6 +58,9 @@ VARIANTS=(
   "symv2|C4:4|f64|$C4 -DPS_TB_SYM_VM=2 -DPS_TB_RB=4 -DPS_TB_NS=3"
   "sym12rb2|C4:4|f64|$C4 -DPS_TB_RB=2 -DPS_TB_NS=4"
   "sym12rb8|C4:4|f64|$C4"
+  "symw8|C4:4|f64|$C4 -DPS_TB_WGS_NW=8"
+  "symw8ns3|C4:4|f64|$C4 -DPS_TB_WGS_NW=8 -DPS_TB_NS=3"
+  "symw8rb4|C4:4|f64|$C4 -DPS_TB_WGS_NW=8 -DPS_TB_NS=3 -DPS_TB_RB=4"
   "c3old2|C3:2|f64|$C3T2 -DPS_TB_SYM=0"
   "c3old3w8|C3:3|f64|$C3T3 -DPS_TB_SYM=0 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8"
   "c3old3w8rb4|C3:3|f64|$C3T3 -DPS_TB_SYM=0 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8 -DPS_TB_RB=4"
