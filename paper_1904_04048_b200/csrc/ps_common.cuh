@@ -370,7 +370,7 @@ constexpr bool tb_wgs() {
   return PS_TB_WGS >= 0 ? PS_TB_WGS != 0
          : tb_vm<T, A, S, TS, PER>() == 2
              ? true
-             : (tb_sym<T, A, S, TS, PER>() ? (PS_TB_SYM_WGS != 0 && !PER)
+             : (tb_sym<T, A, S, TS, PER>() ? (PS_TB_SYM_WGS == 2 || (PS_TB_SYM_WGS != 0 && !PER))
                 : (PS_TB_WGS1 >= 0 ? PS_TB_WGS1 != 0
                                    : ((sizeof(T) == 4 || tb_deep_r2<T, S, TS>()) && !PER)));
 }

@@ -143,9 +143,9 @@ static bool tb_supported(const ps_grid* g, const ps_table* t, int tsteps) {
   // coefficient class (ps_tblock.cuh): the table must give each class one coefficient
   // (every named scheme does); others run unblocked
   const bool ref = g->dtype == PS_F64 || g->arith == PS_ARITH_REF;
-  const bool sym = PS_TB_SYM == 2 ? (ref && (table_radius(t) == 1 || tsteps <= PS_TB_SYM_R2_MAXT))
-                   : PS_TB_SYM == 1 ? (g->dtype == PS_F64 && table_radius(t) == 1 &&
-                                       g->bc == PS_BC_DIRICHLET)
+  const bool fits = table_radius(t) == 1 || tsteps <= PS_TB_SYM_R2_MAXT;
+  const bool sym = PS_TB_SYM == 2   ? (ref && fits)
+                   : PS_TB_SYM == 1 ? (g->dtype == PS_F64 && g->bc == PS_BC_DIRICHLET && fits)
                                     : false;
   if (sym) {
     const bool eq = shape_matches<ShapeP5>(t)   ? tb_classes_equal<ShapeP5>(t)

@@ -203,20 +203,23 @@ static bool tb_classes_equal(const ps_table* t) {
 #define PS_TB_SYM 1
 #endif
 // Where the shared-product path is used (measured on B200, tools/tb_tune.sh):
-// f64 radius-1 Dirichlet passes (C4: 652 vs 651 GLUP/s at 1965 MHz, 567 vs 558 under the
-// power cap of a 200-step run — 24 % fewer FP64 instructions at equal time shows the pass
-// is bound by DRAM traffic and issue slots, not by the FP64 pipe).  Not used for periodic
-// grids (11 consumer warps x 168 registers spill: C2 252 vs 288-346), radius 2 (the state
-// of three stages needs 8 x 232-register warps: C3 T=3 385 vs 381) or the f32 reference
-// contract (C5 286 vs 287): PS_TB_SYM=2 forces it everywhere it can compile.
+// every f64 Dirichlet pass whose state fits 8 warpgroup-specialised consumer warps x 232
+// registers without spilling: radius 1 at any depth up to 6, radius 2 up to depth 3.
+//   C4 (P9, T=4, 200-240 steps under the power cap): 600-605 vs 557 GLUP/s for one product
+//   per tap (FP64 instructions per update 19 -> 13); depth 5 — 15 doubles of state per
+//   stage is what lets five stages fit — 638; C3 (P13, T=3): 423 vs 382.
+// Not used where it measured no better: periodic grids (C2 259 vs 260), the f32 reference
+// contract (C5 286 vs 287), radius 2 at depth 4 (1.2 KB of spills: 97-231 vs 360).
+// PS_TB_SYM=2 forces it everywhere it can compile, PS_TB_SYM=0 removes it.
 #ifndef PS_TB_SYM_R2_MAXT
-#define PS_TB_SYM_R2_MAXT 2  // radius 2 under PS_TB_SYM=2: deepest fusion that fits
+#define PS_TB_SYM_R2_MAXT 3  // radius 2: deepest fusion whose shared-product state fits
 #endif
 template <typename T, int A, class S, int TS, bool PER>
 __host__ __device__ constexpr bool tb_sym() {
   if (PS_TB_SYM == 0 || !Arith<T, A>::kSplit || !sym_shape<S>()) return false;
-  if (PS_TB_SYM == 2) return S::R == 1 || TS <= PS_TB_SYM_R2_MAXT;
-  return sizeof(T) == 8 && S::R == 1 && !PER;
+  if (S::R > 1 && TS > PS_TB_SYM_R2_MAXT) return false;
+  if (PS_TB_SYM == 2) return true;
+  return sizeof(T) == 8 && !PER;
 }
 
 // HALO: Dirichlet row slab whose boundary rows also go to the neighbours (a separate

@@ -51,24 +51,22 @@ C4="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=4"
 C3T2="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=2"
 C3T3="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=3"
 C3T4="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=4"
+C2T4="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=4 -DPS_TUNE_BC=PS_BC_PERIODIC"
+C2T5="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=5 -DPS_TUNE_BC=PS_BC_PERIODIC"
+C5T4="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=4"
 VARIANTS=(
-  "old|C4:4|f64|$C4 -DPS_TB_SYM=0"
-  "sym12|C4:4|f64|$C4 -DPS_TB_RB=4 -DPS_TB_NS=3"
-  "sym11|C4:4|f64|$C4 -DPS_TB_SYM_WGS=0 -DPS_TB_RB=4 -DPS_TB_NS=3"
-  "symv2|C4:4|f64|$C4 -DPS_TB_SYM_VM=2 -DPS_TB_RB=4 -DPS_TB_NS=3"
-  "sym12rb2|C4:4|f64|$C4 -DPS_TB_RB=2 -DPS_TB_NS=4"
-  "sym12rb8|C4:4|f64|$C4"
-  "symw8|C4:4|f64|$C4 -DPS_TB_WGS_NW=8"
-  "symw8ns3|C4:4|f64|$C4 -DPS_TB_WGS_NW=8 -DPS_TB_NS=3"
-  "symw8rb4|C4:4|f64|$C4 -DPS_TB_WGS_NW=8 -DPS_TB_NS=3 -DPS_TB_RB=4"
-  "c3old2|C3:2|f64|$C3T2 -DPS_TB_SYM=0"
-  "c3old3w8|C3:3|f64|$C3T3 -DPS_TB_SYM=0 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8"
-  "c3old3w8rb4|C3:3|f64|$C3T3 -DPS_TB_SYM=0 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8 -DPS_TB_RB=4"
-  "c3old4w8|C3:4|f64|$C3T4 -DPS_TB_SYM=0 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8 -DPS_TB_RB=5"
-  "c3sym2rb8|C3:2|f64|$C3T2 -DPS_TB_SYM=2 -DPS_TB_RB=8 -DPS_TB_NS=2"
-  "c3sym3w8|C3:3|f64|$C3T3 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=3 -DPS_TB_WGS_NW=8"
-  "c3sym3w8rb8|C3:3|f64|$C3T3 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=3 -DPS_TB_WGS_NW=8 -DPS_TB_RB=8 -DPS_TB_NS=2"
-  "c3sym3w12|C3:3|f64|$C3T3 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=3"
+  "c3sym3a|C3:3|f64|$C3T3 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=3 -DPS_TB_WGS_NW=8 -DPS_TB_RB=8 -DPS_TB_NS=3"
+  "c3sym4a|C3:4|f64|$C3T4 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=4 -DPS_TB_WGS_NW=8 -DPS_TB_RB=8 -DPS_TB_NS=3"
+  "c3sym4b|C3:4|f64|$C3T4 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=4 -DPS_TB_WGS_NW=8 -DPS_TB_RB=4 -DPS_TB_NS=3"
+  "c3old3|C3:3|f64|$C3T3"
+  "c2old4|C2:4|f64|$C2T4"
+  "c2sym4|C2:4|f64|$C2T4 -DPS_TB_SYM=2 -DPS_TB_SYM_WGS=2"
+  "c2sym5|C2:5|f64|$C2T5 -DPS_TB_SYM=2 -DPS_TB_SYM_WGS=2"
+  "c2old4w8|C2:4|f64|$C2T4 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8"
+  "c5base|C5:4|f32n|$C5T4"
+  "c5w8wide|C5:4|f32n|$C5T4 -DPS_TB_WGS_NW=8 -DPS_TB_NARROW=0"
+  "c5w8narrow|C5:4|f32n|$C5T4 -DPS_TB_WGS_NW=8"
+  "c5w8wide8|C5:4|f32n|$C5T4 -DPS_TB_WGS_NW=8 -DPS_TB_NARROW=0 -DPS_TB_RB=8"
 )
 if [ "${MODE:-build}" = build ]; then
   for spec in "${VARIANTS[@]}"; do
@@ -78,7 +76,7 @@ if [ "${MODE:-build}" = build ]; then
     (mkdir -p build/tune/$v &&
      $NV $flags -Xptxas -v -c -o build/tune/$v/$u.o $CSRC/$u.cu > build/tune/$v/ptxas.log 2>&1 &&
      $NV -shared -o build/tune/$v/libps.so $(ls build/obj/*.o | grep -v "/$u.o") build/tune/$v/$u.o &&
-     echo "$v: $(grep -A2 k_two_step_tb build/tune/$v/ptxas.log | grep -E 'spill|Used' | tr '\n' ' ')") &
+     rm -f build/tune/$v/$u.o && echo "$v: $(grep -A2 k_two_step_tb build/tune/$v/ptxas.log | grep -E 'spill|Used' | tr '\n' ' ')") &
   done
   wait
 else
