@@ -65,7 +65,7 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def compute_roofline(cfg, value_glups):
+def compute_roofline(cfg, value_glups, T=1):
     """Arithmetic roofline of the fused kernel (temporal blocking makes it instruction-bound,
     not HBM-bound): FP-pipe instructions per update under the config's contract times the
     update rate, against the DADD (f64) / FFMA (f32) throughput tools/fp64_probe.cu measures
@@ -82,15 +82,28 @@ def compute_roofline(cfg, value_glups):
         rates = json.loads(out.stdout.strip().splitlines()[-1])
     except Exception:
         return None
-    ntaps = len(named_scheme(cfg["scheme"]).two_step)
-    if cfg["dtype"] == "f64":   # reference contract: one DMUL + one DADD per tap, one DSUB
+    spec = named_scheme(cfg["scheme"])
+    ntaps = len(spec.two_step)
+    shared = None
+    if cfg["dtype"] == "f64":
+        # reference sequence: one DMUL + one DADD per tap, one DSUB.  The shared-product
+        # kernels (f64 Dirichlet; radius 2 up to depth 3) multiply once per input element
+        # and coefficient class instead of once per tap: classes + taps + 1 instructions
         ipl, peak, pipe = 2 * ntaps + 1, rates["dadd_rate_32warps_per_sm_Gops"], "fp64"
+        if cfg["bc"] == "dirichlet" and T > 1 and (spec.radius == 1 or T <= 3):
+            classes = len({(abs(q1) + abs(q2), max(abs(q1), abs(q2))) for q1, q2 in spec.two_step})
+            shared = classes + ntaps + 1
     else:                       # native f32: one FFMA per tap, one FADD
         ipl, peak, pipe = ntaps + 1, rates["ffma_rate_Gops"], "fp32"
-    achieved = value_glups * ipl
+    executed = shared or ipl
+    achieved = value_glups * executed
     return {"bound": f"{pipe} pipe", "achieved": achieved, "peak": peak,
             "unit": "G thread-instructions/s", "frac": achieved / peak,
-            "instr_per_lup": ipl,
+            "instr_per_lup": executed, "reference_sequence_instr_per_lup": ipl,
+            **({"shared_products": "one rounded product per input element and coefficient "
+                                   "class feeds every sum that reads it (same bits, "
+                                   f"{ipl - shared} fewer multiplies per update)"}
+               if shared else {}),
             "peak_source": "measured in this run: tools/fp64_probe.cu "
                            f"({'DADD' if pipe == 'fp64' else 'FFMA'} throughput, all SMs)",
             "note": "algorithmic instructions only (no recomputed halo columns/rows); the "
@@ -557,7 +570,7 @@ def gpu_arm_single(args, cfg, cfg_name):
             if cfg["arith"] == "native" else
             "ref = the reference's float32 sequence (f32 products, f64 accumulator), bitwise")
     if T > 1:
-        line["compute_roofline"] = compute_roofline(cfg, m["value"])
+        line["compute_roofline"] = compute_roofline(cfg, m["value"], T)
     if companion:
         line["unblocked_companion"] = companion
     if not args.no_e2e:

@@ -10,13 +10,14 @@ mkdir -p gpurun_out
 for spec in "$@"; do
   cfg="${spec%%:*}"; T="${spec##*:}"
   tag="${cfg}_T${T}"
-  cmd="python bench.py --config $cfg --tsteps $T --steps 8 --warmup 4 --no-e2e --no-cpu"
+  # whole passes only: 4 passes per timed region, one pass of warm-up, one repetition
+  cmd="python bench.py --config $cfg --tsteps $T --steps $((4 * T)) --warmup $T --reps 1 --no-e2e --no-cpu"
   pat="k_two_step_tb"; [ "$T" = 1 ] && pat="k_two_step_stream"
   $cmd > "gpurun_out/bench_${tag}.json" 2> "gpurun_out/bench_${tag}.err" &&
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
       --log-file "gpurun_out/launches_${tag}.csv" $cmd > "gpurun_out/ncu_list_${tag}.log" 2>&1
   $cmd > /dev/null 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k "regex:$pat" -s 3 -c 1 -f \
+  ncu --set full --clock-control none --import-source on -k "regex:$pat" -s 2 -c 1 -f \
       -o "gpurun_out/prof_${tag}" $cmd > "gpurun_out/ncu_full_${tag}.log" 2>&1
   echo "$tag done rc=$?"
 done
