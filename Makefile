@@ -8,8 +8,10 @@ NVFLAGS = -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo \
 CSRC = paper_1904_04048_b200/csrc
 OBJDIR = build/obj
 KERN = f64 f32r f32n
-UNITS = ps_device $(foreach k,$(KERN),ps_kern_$(k) ps_kern_$(k)_t2 ps_kern_$(k)_t3 ps_kern_$(k)_t4) \
-        ps_kern_f64_t5 ps_kern_f64_t6
+# (longest units first: a parallel make starts them in this order)
+UNITS = ps_kern_f64_t5 ps_kern_f64_t6 ps_kern_f64_t4 ps_kern_f64_t3 ps_kern_f32r_t4 ps_kern_f32n_t4 \
+        $(foreach k,$(KERN),ps_kern_$(k)_t2) ps_kern_f32r_t3 ps_kern_f32n_t3 \
+        $(foreach k,$(KERN),ps_kern_$(k)) ps_device
 OBJS = $(addprefix $(OBJDIR)/,$(addsuffix .o,$(UNITS)))
 HDR = include/ps.h $(wildcard $(CSRC)/*.cuh)
 

@@ -26,6 +26,7 @@ struct Arith<double, A> {
   // every output point that reads u through a tap with this coefficient, so the fused
   // kernels compute it once per input element and coefficient class — and the add
   static constexpr bool kSplit = true;
+  static constexpr bool kPair = false;
   __device__ __forceinline__ static acc_t mul(coef_t c, double u) { return __dmul_rn(c, u); }
   __device__ __forceinline__ static acc_t add(acc_t acc, acc_t p) { return __dadd_rn(acc, p); }
   // u^{k+1} = acc - u^{k-1}            (simulator.py:184)
@@ -54,6 +55,7 @@ struct Arith<float, ARITH_REF> {
   __device__ __forceinline__ static acc_t tap(acc_t acc, coef_t c, float u) {
     return __dadd_rn(acc, static_cast<double>(__fmul_rn(c, u)));
   }
+  static constexpr bool kPair = false;
   static constexpr bool kSplit = true;   // product = the f32 product widened once
   __device__ __forceinline__ static acc_t mul(coef_t c, float u) {
     return static_cast<double>(__fmul_rn(c, u));
@@ -84,8 +86,31 @@ struct Arith<float, ARITH_NATIVE> {
     return __fmaf_rn(c, u, acc);
   }
   static constexpr bool kSplit = false;  // one fused operation per tap: nothing to share
+  // Two taps of neighbouring outputs in one instruction: sm_100's packed fma.rn.f32x2 (SASS
+  // FFMA2) performs two independent correctly rounded FMAs on a register pair, with the
+  // coefficient broadcast to both halves — the same bits as two tap() calls for half the
+  // issue slots (the fused f32 kernels are issue-bound, not FMA-pipe-bound).
+  static constexpr bool kPair = true;
+  __device__ __forceinline__ static void tap2(acc_t& a0, acc_t& a1, coef_t c, float u0,
+                                              float u1) {
+    uint64_t ra, ru, rc;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ru) : "f"(u0), "f"(u1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(rc) : "f"(c));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(ra) : "l"(rc), "l"(ru));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(ra));
+  }
   __device__ __forceinline__ static float two(acc_t acc, float ukm1) {
     return __fsub_rn(acc, ukm1);
+  }
+  // two() for a pair of outputs: packed sub.rn.f32x2, the same two rounded subtractions
+  __device__ __forceinline__ static void two2(float& r0, float& r1, acc_t a0, acc_t a1,
+                                              float m0, float m1) {
+    uint64_t ra, rm, rr;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(rm) : "f"(m0), "f"(m1));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(ra), "l"(rm));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rr));
   }
   // first step: acc_u + fl(tau * acc_v) (unfused, so it decomposes like the others)
   __device__ __forceinline__ static float first(acc_t au, acc_t av, float tau) {

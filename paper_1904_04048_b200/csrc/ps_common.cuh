@@ -321,6 +321,9 @@ static ps_status dispatch_two_step_bc(const ps_grid* g, const void* uk, const vo
 #ifndef PS_TUNE_BC
 #define PS_TUNE_BC PS_BC_DIRICHLET
 #endif
+#ifndef PS_TB_RC_ALIGN
+#define PS_TB_RC_ALIGN 1  // 0: keep the round tile heights
+#endif
 #ifndef PS_TB_RB
 #define PS_TB_RB 0  // 0: per radius (launch_tb)
 #endif
@@ -455,7 +458,8 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   p.nstrips = int32_t((g->cols + Gm::W - 1) / Gm::W);
   int rc = env_int("PS_TB_ROW_CHUNK", 0);
   if (rc <= 0) rc = rc_hint;  // banded solve (ps_solve.cuh): its own tile height
-  if (rc <= 0) {
+  const bool rc_auto = rc <= 0;
+  if (rc_auto) {
     const int64_t want_tiles = int64_t(resident) * 8;
     const int64_t chunks = (want_tiles + p.nstrips - 1) / p.nstrips;
     rc = int(std::max<int64_t>(1, (nrows + chunks - 1) / chunks));
@@ -469,6 +473,10 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
         break;
       }
   }
+  // a tile streams rc + 2*R*TS rows: make that a whole number of pipeline slots, so the
+  // tile's last slot is a full (unrolled) one
+  if (PS_TB_RC_ALIGN && rc_auto && rc >= 8 * RB)
+    rc += (RB - (rc + 2 * S::R * TS) % RB) % RB;
   rc = int(std::min<int64_t>(rc, nrows));
   p.rc = rc;
   p.ntiles = int32_t(((nrows + rc - 1) / rc) * p.nstrips);
@@ -525,16 +533,17 @@ static ps_status dispatch_tb(const ps_grid* g, const void* uk, const void* ukm1,
     if (shape_matches<ShapeP9>(t)) return go(ShapeP9{});
     if (shape_matches<ShapeC9>(t)) return go(ShapeC9{});
     return PS_ERR_TABLE;
+  } else {  // (an else branch, so depths 5 and 6 do not instantiate the kernels below)
+    if (shape_matches<ShapeP5>(t))
+      return launch_tb_bc<T, A, TS, ShapeP5>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    if (shape_matches<ShapeP9>(t))
+      return launch_tb_bc<T, A, TS, ShapeP9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    if (shape_matches<ShapeC9>(t))
+      return launch_tb_bc<T, A, TS, ShapeC9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    if (shape_matches<ShapeP13>(t))
+      return launch_tb_bc<T, A, TS, ShapeP13>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
+    return PS_ERR_TABLE;
   }
-  if (shape_matches<ShapeP5>(t))
-    return launch_tb_bc<T, A, TS, ShapeP5>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
-  if (shape_matches<ShapeP9>(t))
-    return launch_tb_bc<T, A, TS, ShapeP9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
-  if (shape_matches<ShapeC9>(t))
-    return launch_tb_bc<T, A, TS, ShapeC9>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
-  if (shape_matches<ShapeP13>(t))
-    return launch_tb_bc<T, A, TS, ShapeP13>(g, uk, ukm1, op, ol, t, lo, hi, st, rev, rc, h);
-  return PS_ERR_TABLE;
 #endif
 }
 

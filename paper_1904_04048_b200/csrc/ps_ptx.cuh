@@ -49,6 +49,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Producer-side wait: sleeps between polls, so the spinning producer warp does not take
+// issue slots from the consumer warps of its SM sub-partition (the ring is slots ahead, a
+// few hundred ns of refill delay are free).
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) {
+    if (ns) __nanosleep(ns);
+  }
+}
+
 // One TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 // dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,

@@ -77,6 +77,14 @@ __device__ __forceinline__ T shfl_down1(T x) {
   return __shfl_down_sync(0xffffffffu, x, 1);
 }
 
+#ifndef PS_TB_PROD_SLEEP
+#define PS_TB_PROD_SLEEP 100  // ns the producer sleeps between polls of a ring slot's release
+#endif
+#ifndef PS_TB_SYM_EDGE
+#define PS_TB_SYM_EDGE 1  // shared-product kernels: unrolled body for full ring-adjacent slots
+                          // (1: plain radius-1 passes up to depth 5 — the radius-2 unit
+                          // takes 8 min to compile with it; 2: every instance)
+#endif
 #ifndef PS_TB_MINB
 #define PS_TB_MINB 0  // tuning override: minimum resident blocks per SM (caps registers)
 #endif
@@ -123,6 +131,17 @@ __device__ __forceinline__ void st_pred(T* dst, const T* res, bool pred) {
     }
   }
 }
+
+// Parity of the window column (R + q2) most taps start on: those taps run as packed pairs.
+template <class S>
+__host__ __device__ constexpr int pair_parity() {
+  int n[2] = {0, 0};
+  for (int s = 0; s < S::N; ++s) ++n[(S::R + S::q(s, 1)) & 1];
+  return n[1] > n[0] ? 1 : 0;
+}
+#ifndef PS_TB_PAIR
+#define PS_TB_PAIR 1  // native f32: FFMA2 for the taps on the majority column parity (0: off)
+#endif
 
 // Largest |q2| among the taps of row offset d (how many neighbour columns it reads).
 template <class S>
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
     if ((!WGS || warp == 0) && lane == 0) {
       while (!P.done) {
         const uint32_t k = P.g / NS;
-        if (k > 0) mbar_wait(&empty[P.g % NS], (k - 1) & 1);
+        if (k > 0) mbar_wait_backoff(&empty[P.g % NS], (k - 1) & 1, PS_TB_PROD_SLEEP);
         prod_issue(P);
       }
     }
@@ -409,19 +428,49 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
       }
     }
     acc_t acc[V];
+    if constexpr (Ar::kPair && PS_TB_PAIR != 0 && V % 2 == 0) {
+      // packed taps: window columns (x, x+1) with x of the parity most taps start on are
+      // register pairs, and every tap starting on that parity updates two outputs with one
+      // FFMA2; the other taps stay scalar.  Each output still sees its taps in table order.
+      constexpr int par = pair_parity<S>();
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      acc_t a = Ar::zero();
+      for (int v = 0; v < V; ++v) acc[v] = Ar::zero();
 #pragma unroll
-      for (int s = 0; s < S::N; ++s)
-        a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
-      acc[v] = a;
+      for (int s = 0; s < S::N; ++s) {
+        const int x0 = R + S::q(s, 1);
+        if ((x0 & 1) == par) {
+#pragma unroll
+          for (int v = 0; v < V; v += 2)
+            Ar::tap2(acc[v], acc[v + 1], c[s], win[t][R + S::q(s, 0)][x0 + v],
+                     win[t][R + S::q(s, 0)][x0 + v + 1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            acc[v] = Ar::tap(acc[v], c[s], win[t][R + S::q(s, 0)][x0 + v]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        acc_t a = Ar::zero();
+#pragma unroll
+        for (int s = 0; s < S::N; ++s)
+          a = Ar::tap(a, c[s], win[t][R + S::q(s, 0)][R + v + S::q(s, 1)]);
+        acc[v] = a;
+      }
     }
     if constexpr (PER || INTERIOR) {
       // periodic (ghosts hold valid images) or a slot whose rows and strip are all off
       // the Dirichlet ring: nothing to mask
+      // (packed when the own columns start a register pair of the window)
+      if constexpr (Ar::kPair && PS_TB_PAIR != 0 && V % 2 == 0 && (R & 1) == pair_parity<S>()) {
 #pragma unroll
-      for (int v = 0; v < V; ++v) res[v] = Ar::two(acc[v], minus[v]);
+        for (int v = 0; v < V; v += 2)
+          Ar::two2(res[v], res[v + 1], acc[v], acc[v + 1], minus[v], minus[v + 1]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) res[v] = Ar::two(acc[v], minus[v]);
+      }
       return;
     }
     const int gi = p.row0 + row;
@@ -745,6 +794,13 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
 #pragma unroll
         for (int mm = 0; mm < RB; ++mm)
           sym_row(std::true_type{}, std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
+                  j0, cols_inner, lane_store);
+      } else if ((PS_TB_SYM_EDGE == 2 || (PS_TB_SYM_EDGE == 1 && R == 1 && !HALO && TS <= 5)) && steady) {
+        // full slots touching the Dirichlet ring (first/last strips and chunks): unrolled
+        // too, masks and plain stores kept
+#pragma unroll
+        for (int mm = 0; mm < RB; ++mm)
+          sym_row(std::true_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
                   j0, cols_inner, lane_store);
       } else {
         // tile heads/tails and slots touching the ring (or the image bands): one rolled

@@ -54,7 +54,17 @@ C3T4="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=4"
 C2T4="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=4 -DPS_TUNE_BC=PS_BC_PERIODIC"
 C2T5="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=5 -DPS_TUNE_BC=PS_BC_PERIODIC"
 C5T4="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=4"
+C4T5="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=5"
 VARIANTS=(
+  "c4t5base|C4:5|f64|$C4T5"
+  "c4t5sleep|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100"
+  "c4t5sleep4|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=400"
+  "c4t5edge|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_SYM_EDGE=1 -DPS_TB_RC_ALIGN=1"
+  "c4t5align|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_RC_ALIGN=1"
+  "c5sleep|C5:4|f32n|$C5T4 -DPS_TB_PROD_SLEEP=100"
+  "c5pair|C5:4|f32n|$C5T4 -DPS_TB_PAIR=1"
+  "c5nopair|C5:4|f32n|$C5T4 -DPS_TB_PAIR=0"
+  "c3t3sleep|C3:3|f64|$C3T3 -DPS_TB_PROD_SLEEP=100"
   "c3sym3a|C3:3|f64|$C3T3 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=3 -DPS_TB_WGS_NW=8 -DPS_TB_RB=8 -DPS_TB_NS=3"
   "c3sym4a|C3:4|f64|$C3T4 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=4 -DPS_TB_WGS_NW=8 -DPS_TB_RB=8 -DPS_TB_NS=3"
   "c3sym4b|C3:4|f64|$C3T4 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=4 -DPS_TB_WGS_NW=8 -DPS_TB_RB=4 -DPS_TB_NS=3"
