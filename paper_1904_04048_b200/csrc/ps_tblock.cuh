@@ -82,8 +82,7 @@ __device__ __forceinline__ T shfl_down1(T x) {
 #endif
 #ifndef PS_TB_SYM_EDGE
 #define PS_TB_SYM_EDGE 1  // shared-product kernels: unrolled body for full ring-adjacent slots
-                          // (1: plain radius-1 passes up to depth 5 — the radius-2 unit
-                          // takes 8 min to compile with it; 2: every instance)
+                          // (1: plain passes up to depth 5; 2: every instance)
 #endif
 #ifndef PS_TB_MINB
 #define PS_TB_MINB 0  // tuning override: minimum resident blocks per SM (caps registers)
@@ -795,13 +794,18 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
         for (int mm = 0; mm < RB; ++mm)
           sym_row(std::true_type{}, std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
                   j0, cols_inner, lane_store);
-      } else if ((PS_TB_SYM_EDGE == 2 || (PS_TB_SYM_EDGE == 1 && R == 1 && !HALO && TS <= 5)) && steady) {
+      } else if ((PS_TB_SYM_EDGE == 2 || (PS_TB_SYM_EDGE == 1 && !HALO && TS <= 5)) && steady) {
         // full slots touching the Dirichlet ring (first/last strips and chunks): unrolled
-        // too, masks and plain stores kept
+        // too, masks and plain stores kept (C4 +2 %, C3 +8 %).  Radius 2 unrolls one 2R-row
+        // rotation of the delay lines at a time: the 8-row body takes ptxas 8 minutes.
+        constexpr int EU = (R == 1 || RB % (2 * R) != 0) ? RB : 2 * R;
+#pragma unroll 1
+        for (int m0 = 0; m0 < RB; m0 += EU) {
 #pragma unroll
-        for (int mm = 0; mm < RB; ++mm)
-          sym_row(std::true_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
-                  j0, cols_inner, lane_store);
+          for (int mm = 0; mm < EU; ++mm)
+            sym_row(std::true_type{}, std::false_type{}, su + (m0 + mm) * LU, sk + (m0 + mm) * LK,
+                    mlo + m0 + mm, i0, i1, j0, cols_inner, lane_store);
+        }
       } else {
         // tile heads/tails and slots touching the ring (or the image bands): one rolled
         // body with every check (a few percent of the slots on the large grids)

@@ -62,6 +62,7 @@ VARIANTS=(
   "c4t5edge|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_SYM_EDGE=1 -DPS_TB_RC_ALIGN=1"
   "c4t5align|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_RC_ALIGN=1"
   "c5sleep|C5:4|f32n|$C5T4 -DPS_TB_PROD_SLEEP=100"
+  "c3t3edge|C3:3|f64|$C3T3 -DPS_TB_SYM_EDGE=2"
   "c5pair|C5:4|f32n|$C5T4 -DPS_TB_PAIR=1"
   "c5nopair|C5:4|f32n|$C5T4 -DPS_TB_PAIR=0"
   "c3t3sleep|C3:3|f64|$C3T3 -DPS_TB_PROD_SLEEP=100"
