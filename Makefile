@@ -29,6 +29,11 @@ build/fp64_probe: tools/fp64_probe.cu
 	@mkdir -p build
 	$(NVCC) -O3 -gencode arch=compute_100a,code=sm_100a -o $@ $<
 
+# issue-slot probe (does an FP64 instruction leave room for others?): profiles/r02_issue_probe.jsonl
+build/issue_probe: tools/issue_probe.cu
+	@mkdir -p build
+	$(NVCC) -O3 -gencode arch=compute_100a,code=sm_100a -o $@ $<
+
 oracle:
 	$(MAKE) -C oracle
 

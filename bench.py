@@ -127,7 +127,9 @@ class ClockSampler:
     BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
             "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, gpu: str, period_s: float = 0.004):
+    def __init__(self, gpu: str, period_s: float | None = None):
+        if period_s is None:
+            period_s = float(os.environ.get("PS_BENCH_CLOCK_PERIOD_MS", "4")) * 1e-3
         self.gpu, self.period = gpu, period_s
         self.sm, self.mx, self.reasons = [], [], set()
         self.stop = threading.Event()

@@ -84,6 +84,11 @@ __device__ __forceinline__ T shfl_down1(T x) {
 #define PS_TB_SYM_EDGE 1  // shared-product kernels: unrolled body for full ring-adjacent slots
                           // (1: plain passes up to depth 5; 2: every instance)
 #endif
+#ifndef PS_TB_SYM_HEAD
+#define PS_TB_SYM_HEAD 0  // unrolled body for a tile's head slots: 1 = C3 kernel only, 2 = all
+                          // (off: C3 f64 T=3 451 -> 458 GLUP/s, C4 within noise, but ptxas
+                          // needs 7 more minutes for the second 8-row radius-2 body)
+#endif
 #ifndef PS_TB_MINB
 #define PS_TB_MINB 0  // tuning override: minimum resident blocks per SM (caps registers)
 #endif
@@ -551,17 +556,21 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
         put(static_cast<T*>(hd) + int64_t(row - p.rows) * pitch + gc0, gc0, res);
     }
     if constexpr (PER) {
-      // refresh wrap-around images to depth D = R*TS (what the next pass loads)
+      // refresh wrap-around images to depth D = R*TS (what the next pass loads).  Two
+      // copies with constant trip counts, selected once by row_images: a run-time loop
+      // bound here kept the image loop rolled and cost the periodic pass 25 % (C2 347 ->
+      // 262 GLUP/s between two round-2 commits).
       const int D = R * TS;
-      const int ri = p.row_images;
-      const bool erow = ri && ((row < D) || (row >= p.rows - D));
       const bool ecol = (gc0 < D) || (gc0 + V > p.cols - D);
-      if (erow || ecol) {
+      auto images = [&](auto rows_tag) {
+        constexpr int RI = decltype(rows_tag)::value ? 1 : 0;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const int j = gc0 + v;
           if (j >= p.cols) continue;
-          for (int a = -ri; a <= ri; ++a)
+#pragma unroll
+          for (int a = -RI; a <= RI; ++a)
+#pragma unroll
             for (int b = -1; b <= 1; ++b) {
               if (a == 0 && b == 0) continue;
               const int ii = row + a * p.rows;
@@ -570,6 +579,11 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
               base[int64_t(ii) * pitch + jj] = res[v];
             }
         }
+      };
+      if (p.row_images) {
+        if ((row < D) || (row >= p.rows - D) || ecol) images(std::true_type{});
+      } else if (ecol) {
+        images(std::false_type{});
       }
     }
   };
@@ -705,9 +719,17 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
       }
     };
 
-    auto sym_row = [&](auto steady_tag, auto interior_tag, const T* su_row, const T* sk_row,
-                       int m, int i0, int i1, int j0, bool cols_inner, bool lane_store) {
+    // head_tag: the STEADY body run while the pipeline is still filling (a tile's first
+    // slots): every stage runs on whatever its state holds, rows above the tile are never
+    // stored, and a stage's state is all valid rows again 2R calls after its input is
+    // (sums restart every row, delay lines are 2R rows deep) -- exactly when the rolled
+    // body would have switched the stage on.
+    auto sym_row = [&](auto steady_tag, auto interior_tag, auto head_tag, const T* su_row,
+                       const T* sk_row, int m, int i0, int i1, int j0, bool cols_inner,
+                       bool lane_store) {
       constexpr bool STEADY = decltype(steady_tag)::value;
+      constexpr bool HEAD = decltype(head_tag)::value;
+      static_assert(!HEAD || STEADY, "head slots run the steady body");
       const int e = i0 - R * TS + m;
       const int gc0 = j0 + gc_lane;
       T own[V], nl[VV], nr[VV], res[V], minus[V], oldest[V];
@@ -738,7 +760,8 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
         constexpr bool PRED_ST = STEADY && decltype(interior_tag)::value && !HALO;
         if constexpr (t == TS - 1) {
           if constexpr (PRED_ST)
-            st_pred<T, VM>(out_last + int64_t(row) * pitch + gc0, res, lane_store);
+            st_pred<T, VM>(out_last + int64_t(row) * pitch + gc0, res,
+                           lane_store && (!HEAD || row >= i0));
           else if (lane_store && (STEADY || (row >= i0 && row < i1)))
             store_vec(out_last, row, gc0, res, true);
         } else {
@@ -792,8 +815,18 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
       if (steady && interior) {
 #pragma unroll
         for (int mm = 0; mm < RB; ++mm)
-          sym_row(std::true_type{}, std::true_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0, i1,
-                  j0, cols_inner, lane_store);
+          sym_row(std::true_type{}, std::true_type{}, std::false_type{}, su + mm * LU,
+                  sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner, lane_store);
+      } else if ((PS_TB_SYM_HEAD == 2 || (PS_TB_SYM_HEAD == 1 && R == 2 && TS == 3)) && !HALO &&
+                 !PER && interior && mlo + RB <= ne) {
+        // a full head slot of a tile off the ring: the unrolled body with row-checked stores
+        // instead of the rolled one (2 of a tile's slots, ~3x the steady cost each).  Only
+        // where it measured a gain worth a second copy of the unrolled body: C3 f64 T=3
+        // 451 -> 458 GLUP/s; C4 T=5 within noise (750 vs 728-758) for twice the compile time.
+#pragma unroll
+        for (int mm = 0; mm < RB; ++mm)
+          sym_row(std::true_type{}, std::true_type{}, std::true_type{}, su + mm * LU,
+                  sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner, lane_store);
       } else if ((PS_TB_SYM_EDGE == 2 || (PS_TB_SYM_EDGE == 1 && !HALO && TS <= 5)) && steady) {
         // full slots touching the Dirichlet ring (first/last strips and chunks): unrolled
         // too, masks and plain stores kept (C4 +2 %, C3 +8 %).  Radius 2 unrolls one 2R-row
@@ -803,16 +836,16 @@ __global__ void __launch_bounds__((NW + (WGS ? 4 : 1)) * 32, (tb_minb<T, S, TS, 
         for (int m0 = 0; m0 < RB; m0 += EU) {
 #pragma unroll
           for (int mm = 0; mm < EU; ++mm)
-            sym_row(std::true_type{}, std::false_type{}, su + (m0 + mm) * LU, sk + (m0 + mm) * LK,
-                    mlo + m0 + mm, i0, i1, j0, cols_inner, lane_store);
+            sym_row(std::true_type{}, std::false_type{}, std::false_type{}, su + (m0 + mm) * LU,
+                    sk + (m0 + mm) * LK, mlo + m0 + mm, i0, i1, j0, cols_inner, lane_store);
         }
       } else {
         // tile heads/tails and slots touching the ring (or the image bands): one rolled
         // body with every check (a few percent of the slots on the large grids)
 #pragma unroll 1
         for (int mm = 0; mm < min(RB, ne - mlo); ++mm)
-          sym_row(std::false_type{}, std::false_type{}, su + mm * LU, sk + mm * LK, mlo + mm, i0,
-                  i1, j0, cols_inner, lane_store);
+          sym_row(std::false_type{}, std::false_type{}, std::false_type{}, su + mm * LU,
+                  sk + mm * LK, mlo + mm, i0, i1, j0, cols_inner, lane_store);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

@@ -57,6 +57,9 @@ C5T4="-DPS_TUNE_SHAPE=ShapeP13 -DPS_TUNE_TS=4"
 C4T5="-DPS_TUNE_SHAPE=ShapeP9 -DPS_TUNE_TS=5"
 VARIANTS=(
   "c4t5base|C4:5|f64|$C4T5"
+  "c4t5nohead|C4:5|f64|$C4T5 -DPS_TB_SYM_HEAD=0"
+  "c3t3base|C3:3|f64|$C3T3"
+  "c3t3nohead|C3:3|f64|$C3T3 -DPS_TB_SYM_HEAD=0"
   "c4t5sleep|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100"
   "c4t5sleep4|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=400"
   "c4t5edge|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_SYM_EDGE=1 -DPS_TB_RC_ALIGN=1"
@@ -71,6 +74,7 @@ VARIANTS=(
   "c3sym4b|C3:4|f64|$C3T4 -DPS_TB_SYM=2 -DPS_TB_SYM_R2_MAXT=4 -DPS_TB_WGS_NW=8 -DPS_TB_RB=4 -DPS_TB_NS=3"
   "c3old3|C3:3|f64|$C3T3"
   "c2old4|C2:4|f64|$C2T4"
+  "c2sleep0|C2:4|f64|$C2T4 -DPS_TB_PROD_SLEEP=0"
   "c2sym4|C2:4|f64|$C2T4 -DPS_TB_SYM=2 -DPS_TB_SYM_WGS=2"
   "c2sym5|C2:5|f64|$C2T5 -DPS_TB_SYM=2 -DPS_TB_SYM_WGS=2"
   "c2old4w8|C2:4|f64|$C2T4 -DPS_TB_WGS=1 -DPS_TB_WGS_NW=8"
