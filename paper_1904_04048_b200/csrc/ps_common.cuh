@@ -411,7 +411,12 @@ static ps_status launch_tb(const ps_grid* g, const void* uk, const void* ukm1, v
   // 8 or 10 rows no longer fit the shared memory)
   // shared-product kernels rotate 2R-row delay lines: a multiple of 2R rows per slot
   // (8 warps: 8 rows x 3 slots 664-692 GLUP/s on C4, 8 x 2 573-583, 4 x 3 603-606)
-  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? 8 : (S::R == 2 ? 6 : 2 * S::R + 1);
+  // radius 1: 10 rows x 3 slots where they fit the 227 KB (depths >= 4: narrower strips) --
+  // C4 T=5 772 vs 756 GLUP/s at full clocks (6 x 4: 737, 4 x 6: 718: the per-slot
+  // wait/arrive round is what costs, so fewer, taller slots)
+  constexpr int RBS =
+      (S::R == 1 && TBGeom<T, NW, 10, NS, S::R, TS, VM>::smem_bytes <= size_t(227) * 1024) ? 10 : 8;
+  constexpr int RB = PS_TB_RB > 0 ? PS_TB_RB : SYM ? RBS : (S::R == 2 ? 6 : 2 * S::R + 1);
   using Gm = TBGeom<T, NW, RB, NS, S::R, TS, VM>;
   auto kern = k_two_step_tb<T, A, S, TS, PER, HALO, NW, RB, NS, VM, WGS>;
   static std::once_flag once[kMaxDevices];

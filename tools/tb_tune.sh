@@ -60,6 +60,11 @@ VARIANTS=(
   "c4t5nohead|C4:5|f64|$C4T5 -DPS_TB_SYM_HEAD=0"
   "c3t3base|C3:3|f64|$C3T3"
   "c3t3nohead|C3:3|f64|$C3T3 -DPS_TB_SYM_HEAD=0"
+  "c4t5_4x6|C4:5|f64|$C4T5 -DPS_TB_RB=4 -DPS_TB_NS=6"
+  "c4t5_6x4|C4:5|f64|$C4T5 -DPS_TB_RB=6 -DPS_TB_NS=4"
+  "c4t5_2x12|C4:5|f64|$C4T5 -DPS_TB_RB=2 -DPS_TB_NS=12"
+  "c4t5_10x3|C4:5|f64|$C4T5 -DPS_TB_RB=10 -DPS_TB_NS=3"
+  "c4t5_sleep0|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=0"
   "c4t5sleep|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100"
   "c4t5sleep4|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=400"
   "c4t5edge|C4:5|f64|$C4T5 -DPS_TB_PROD_SLEEP=100 -DPS_TB_SYM_EDGE=1 -DPS_TB_RC_ALIGN=1"
