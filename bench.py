@@ -34,7 +34,7 @@ METRIC = "grid-point updates/sec (GLUP/s) and fraction of HBM roofline, 1/2/4/8 
 
 CONFIGS = {
     "C1": dict(scheme="P5", n=511, bc="dirichlet", ring=1, dtype="f64", arith="ref", lam=0.5,
-               steps=200, ic="gauss-centre",
+               steps=200, ic="gauss-centre", tile=12,
                desc="C1: P5 5-point, 512^2 f64, Dirichlet ring 1, lambda=0.5, 200 steps"),
     "C2": dict(scheme="P9", n=4096, bc="periodic", ring=0, dtype="f64", arith="ref", lam=0.6,
                steps=1000, ic="standing", tb=4,
@@ -406,12 +406,12 @@ def reference_arm(args, cfg, cfg_name):
 
 
 # ------------------------------------------------------------------------------ GPU arm
-def make_sim(cfg, tsteps=1):
+def make_sim(cfg, tsteps=1, tile=0):
     from paper_1904_04048_b200.device import Simulation
 
     sim = Simulation(cfg["scheme"], cfg["n"], cfg["lam"], bc=cfg["bc"],
                      ring=cfg["ring"] if cfg["bc"] == "dirichlet" else None,
-                     dtype=cfg["dtype"], arith=cfg["arith"], tsteps=tsteps)
+                     dtype=cfg["dtype"], arith=cfg["arith"], tsteps=tsteps, tile=tile)
     ic = cfg["ic"]
     if ic == "standing":
         sim.standing_wave_initial(4, 6)
@@ -428,7 +428,7 @@ def make_sim(cfg, tsteps=1):
     return sim
 
 
-def measure_march(args, cfg, T):
+def measure_march(args, cfg, T, tile=0):
     """Build the config's grid, first step, warm up, then time K march steps at temporal
     blocking depth T with CUDA events on the launching stream.  The K-step region is
     repeated (``--reps``; auto: 3 while one region takes under 2 s) and the MEDIAN region is
@@ -437,15 +437,17 @@ def measure_march(args, cfg, T):
 
     from paper_1904_04048_b200 import _native as nat
 
-    sim = make_sim(cfg, T)
+    sim = make_sim(cfg, T, tile)
     sim.first_step()
     stream = torch.cuda.current_stream()
     K = args.steps
     warm = args.warmup
     if warm:
         sim.march(warm)
+    # ps_march_tile: ONE launch runs all K updates
+    tiled = bool(sim.tile) and nat.tile_supported(sim.grid, sim.t_two, sim.tile)
     extra = None
-    if T == 1 and K >= 12:
+    if T == 1 and K >= 12 and not tiled:
         # ps_march replays a CUDA graph for calls of >= 12 steps; instantiate it outside
         # the timed region with one extra 12-step call (reported, not hidden in `warmup`)
         sim.march(12)
@@ -471,6 +473,9 @@ def measure_march(args, cfg, T):
     total_ms = statistics.median(regions)
     lup_step = sim.updated_nodes
     avg_launch_ms = total_ms / K * T      # K/T launches of T fused updates each
+    if tiled:
+        T = K                             # accounting below: one launch of K updates
+        avg_launch_ms = total_ms
     peak, peak_src = load_peak()
     # algorithmic traffic = 3 words per update (read u^k, u^{k-1}, write
     # u^{k+1}); a launch of depth T performs T * lup_step updates
@@ -480,7 +485,7 @@ def measure_march(args, cfg, T):
     # and writes two for T updates (4/T words per update); T = 1 moves the 3 words
     dram_words = 3.0 if T == 1 else 4.0 / T
     dram_model = dram_words * T * sim.itemsize * lup_step
-    return {"sim": sim, "T": T, "K": K, "warmup": warm, "warmup_extra": extra,
+    return {"sim": sim, "T": T, "K": K, "warmup": warm, "warmup_extra": extra, "tiled": tiled,
             "total_ms": total_ms, "regions_ms": regions,
             "value": lup_step * K / (total_ms * 1e-3) / 1e9, "launches": launches,
             "clocks": clk.summary(), "lup_step": lup_step, "bytes_launch": bytes_launch,
@@ -540,9 +545,27 @@ def gpu_arm_single(args, cfg, cfg_name):
                      "warmup_extra": c1["warmup_extra"], "clocks": c1["clocks"]}
         del c1
         torch.cuda.empty_cache()
-    m = measure_march(args, cfg, T)
+    tile = args.tile if args.tile >= 0 else (cfg.get("tile", 0) if T == 1 else 0)
+    if tile and args.tile < 0:
+        # also time the streaming march (one CUDA-graph-replayed launch per update)
+        c1 = measure_march(args, cfg, 1)
+        r1, d1 = roofline_block(c1, cfg_name)
+        companion = {"what": "streaming march: one launch per update, CUDA-graph replay + PDL",
+                     "value": c1["value"], "unit": "GLUP/s",
+                     "ms_per_step": c1["total_ms"] / c1["K"], "roofline_frac": r1["frac"],
+                     "regions_ms": c1["regions_ms"], "warmup_extra": c1["warmup_extra"],
+                     "clocks": c1["clocks"]}
+        del c1
+        torch.cuda.empty_cache()
+    m = measure_march(args, cfg, T, tile)
     sim = m["sim"]
     roof, dram = roofline_block(m, cfg_name)
+    if m["tiled"]:
+        note = ("tile-resident march (ps_march_tile): ONE cooperative launch runs all the "
+                f"region's updates, {tile} per shared-memory pass; levels stay in L2 / shared "
+                "memory, so the 3-words-per-update figure is algorithmic, not DRAM traffic")
+        roof["note"] = note
+        dram = {"note": "L2-resident grid: no DRAM-side model (see roofline.note)"}
     line = {
         "metric": METRIC, "value": m["value"], "unit": "GLUP/s", "n_gpus": 1, "steps": m["K"],
         "warmup": m["warmup"], "ms_per_step": m["total_ms"] / m["K"], "higher_is_better": True,
@@ -551,6 +574,7 @@ def gpu_arm_single(args, cfg, cfg_name):
         "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
                    "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
                    "parallelism": "single GPU", "temporal_blocking": T,
+                   "tile_resident_depth": tile if m["tiled"] else 0,
                    "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
                          "streamed from HBM every launch" if sim.level_bytes > 126e6 else
                          "grid fits in L2 (latency-bound correctness config)"},
@@ -898,6 +922,9 @@ def main():
     ap.add_argument("--reps", type=int, default=0,
                     help="repetitions of the K-step timed region (median reported); 0 = auto: "
                          "3 while a region takes under 2 s, else 1")
+    ap.add_argument("--tile", type=int, default=-1,
+                    help="tile-resident march depth for small Dirichlet f64 grids (ps_march_tile); "
+                         "-1 = the config's default (C1: 12, with a streaming companion), 0 = off")
     ap.add_argument("--tsteps", type=int, default=0, choices=(0, 1, 2, 3, 4, 5, 6),
                     help="temporal blocking depth; 0 = the config's measured best (C4: 5; C2, C5 "
                          "and C3 f32: 4; C3 f64: 3; with an unblocked companion measurement; "

@@ -205,6 +205,20 @@ ps_status ps_two_step_tb_halo(const ps_grid* g, const void* uk, const void* ukm1
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
                       int32_t tsteps, int32_t* newest, int32_t* previous, void* stream);
 
+/* Tile-resident march for SMALL Dirichlet f64 grids (a level of at most a few MB: BASELINE
+ * config 1, the reference's own regime — run()'s loop of two_step calls, simulator.py:
+ * 271-274).  One cooperative launch runs all nsteps updates: the grid is cut into one tile
+ * per SM, every pass loads a tile plus a halo of R*tsteps points into shared memory, runs
+ * tsteps updates there and publishes its tile to the other pair of levels; tiles wait only
+ * for their 8 neighbours (release/acquire epoch flags), not for a launch boundary.  Same
+ * level bookkeeping as ps_march_tb (four levels; *newest / *previous updated), same bits
+ * as nsteps ps_two_step calls.  tsteps 1..16.  Returns PS_ERR_ARG when the grid does not
+ * qualify (periodic, f32, row slab, ring narrower than the stencil, or no tiling that fits
+ * the SMs' shared memory): ps_tile_supported() asks first. */
+int32_t ps_tile_supported(const ps_grid* g, const ps_table* t, int32_t tsteps);
+ps_status ps_march_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
+                        int32_t tsteps, int32_t* newest, int32_t* previous, void* stream);
+
 /* Host-to-host solve with the PCIe copies overlapped: the field part
  * of run() (simulator.py:253-282: u0/v0 in, first step, n_t - 1 two-step updates, the
  * final level out; dump_grid_csv's input), from HOST arrays to a HOST array.

@@ -70,7 +70,8 @@ SOLVE_KINDS = ("load", "first", "step", "pass", "store")
 
 EXPORTS = ("ps_layout_init", "ps_slab_layout_init", "ps_level_bytes", "ps_level_alloc", "ps_level_free", "ps_copy_in",
            "ps_copy_out", "ps_fill_ghosts", "ps_first_step", "ps_two_step", "ps_two_step_rows",
-           "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_two_step_halo",
+           "ps_march", "ps_two_step_tb", "ps_two_step_tb_rows", "ps_march_tb", "ps_march_tile",
+           "ps_tile_supported", "ps_two_step_halo",
            "ps_two_step_tb_halo",
            "ps_ipc_get_handle",
            "ps_ipc_open", "ps_ipc_close",
@@ -118,6 +119,9 @@ def load_library(path: str = LIB_PATH):
             "ps_ipc_close": (i32, [vp]),
             "ps_march_tb": (i32, [G, ctypes.POINTER(vp), i64, T, i32, ctypes.POINTER(i32),
                                   ctypes.POINTER(i32), vp]),
+            "ps_march_tile": (i32, [G, ctypes.POINTER(vp), i64, T, i32, ctypes.POINTER(i32),
+                                    ctypes.POINTER(i32), vp]),
+            "ps_tile_supported": (i32, [G, T, i32]),
             "ps_gaussian_sum": (i32, [G, vp, i32, vp, vp, vp, vp, i64, vp]),
             "ps_errsum_create": (vp, [i64, i64]),
             "ps_errsum_step": (i32, [vp, G, vp, vp, dbl, vp, vp]),
@@ -351,6 +355,22 @@ def march_tb(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, pr
     check(load_library().ps_march_tb(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
                                      int(tsteps), ctypes.byref(nw), ctypes.byref(pv),
                                      stream or current_stream()), "ps_march_tb")
+    return nw.value, pv.value
+
+
+def tile_supported(grid, t: PsTable, tsteps: int) -> bool:
+    """True when ps_march_tile can run this grid / table / depth (needs a GPU to ask)."""
+    return bool(load_library().ps_tile_supported(ctypes.byref(grid), ctypes.byref(t), int(tsteps)))
+
+
+def march_tile(grid, levels, nsteps: int, t: PsTable, tsteps: int, newest: int, previous: int,
+               stream=None) -> tuple[int, int]:
+    """ps_march_tile: all ``nsteps`` updates in one cooperative launch (small grids)."""
+    arr = (ctypes.c_void_p * 4)(*[lv.ptr.value for lv in levels])
+    nw, pv = ctypes.c_int32(newest), ctypes.c_int32(previous)
+    check(load_library().ps_march_tile(ctypes.byref(grid), arr, int(nsteps), ctypes.byref(t),
+                                       int(tsteps), ctypes.byref(nw), ctypes.byref(pv),
+                                       stream or current_stream()), "ps_march_tile")
     return nw.value, pv.value
 
 

@@ -57,6 +57,7 @@ static void release_slots(std::vector<int>& slots) {
 
 #include "ps_errsum.cuh"
 #include "ps_batch.cuh"
+#include "ps_tile.cuh"
 
 static ps_status two_step_impl(const ps_grid* g, const void* uk, const void* ukm1, void* ukp1,
                                const ps_table* t, int64_t lo, int64_t hi, cudaStream_t st,
@@ -632,6 +633,80 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
   }
   *newest = cur;
   *previous = prev;
+  return PS_OK;
+}
+
+// Tile-resident march (ps_tile.cuh): 1 = this grid / table / depth can run it.
+static bool tile_plan_for(const ps_grid* g, const ps_table* t, int tsteps, int* py, int* px,
+                          int* th, int* tw, size_t* smem) {
+  if (g->bc != PS_BC_DIRICHLET || g->dtype != PS_F64 || !single_slab(g)) return false;
+  if (tsteps < 1 || tsteps > 16 || !stream_shape(t)) return false;
+  const int R = table_radius(t);
+  if (g->ring < R) return false;
+  return tile_plan(g->rows, g->cols, R, tsteps, std::max(1, dev_info().nsm),
+                   size_t(227) * 1024, py, px, th, tw, smem);
+}
+
+int32_t ps_tile_supported(const ps_grid* g, const ps_table* t, int32_t tsteps) {
+  if (check_grid(g) != PS_OK || !t || check_table(g, t) != PS_OK) return 0;
+  int py, px, th, tw;
+  size_t smem;
+  return tile_plan_for(g, t, tsteps, &py, &px, &th, &tw, &smem) ? 1 : 0;
+}
+
+ps_status ps_march_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
+                        int32_t tsteps, int32_t* newest, int32_t* previous, void* stream) {
+  ps_status s = check_grid(g);
+  if (s != PS_OK) return s;
+  if (!lvl || !newest || !previous || nsteps < 0) return PS_ERR_ARG;
+  const int cur = *newest, prev = *previous;
+  if (cur < 0 || cur > 3 || prev < 0 || prev > 3 || cur == prev) return PS_ERR_ARG;
+  for (int x = 0; x < 4; ++x)
+    if (!lvl[x] || !aligned16(lvl[x])) return lvl[x] ? PS_ERR_ALIGN : PS_ERR_ARG;
+  if ((s = check_table(g, t)) != PS_OK) return s;
+  int py, px, th, tw;
+  size_t smem;
+  if (!tile_plan_for(g, t, tsteps, &py, &px, &th, &tw, &smem)) return PS_ERR_ARG;
+  if (nsteps == 0) return PS_OK;
+  int f1 = -1, f2 = -1;
+  for (int x = 0; x < 4; ++x)
+    if (x != cur && x != prev) (f1 < 0 ? f1 : f2) = x;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // epoch flags: one array out of a per-device ring allocated once (a stream-ordered
+  // allocation per call cost ~1 ms: the default pool hands its memory back at every
+  // synchronisation); 64 marches may be in flight at once before an array is reused
+  constexpr int kFlagSets = 64, kFlagStride = 1024;
+  static unsigned int* flag_pool[kMaxDevices] = {};
+  static std::mutex flag_mu;
+  static std::atomic<unsigned> flag_seq{0};
+  if (size_t(py) * px > size_t(kFlagStride)) return PS_ERR_ARG;
+  unsigned int* flags = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(flag_mu);
+    const int dev = device_index();
+    if (!flag_pool[dev] &&
+        cudaMalloc(reinterpret_cast<void**>(&flag_pool[dev]),
+                   sizeof(unsigned int) * kFlagSets * kFlagStride) != cudaSuccess)
+      return PS_ERR_CUDA;
+    flags = flag_pool[dev] + size_t(flag_seq.fetch_add(1) % kFlagSets) * kFlagStride;
+  }
+#define PS_TILE_GO(S) \
+  launch_tile<S>(g, lvl, nsteps, t, tsteps, cur, prev, f1, f2, flags, st, py, px, th, tw, smem)
+  if (shape_matches<ShapeP5>(t))
+    s = PS_TILE_GO(ShapeP5);
+  else if (shape_matches<ShapeP9>(t))
+    s = PS_TILE_GO(ShapeP9);
+  else if (shape_matches<ShapeC9>(t))
+    s = PS_TILE_GO(ShapeC9);
+  else
+    s = PS_TILE_GO(ShapeP13);
+#undef PS_TILE_GO
+  if (s != PS_OK) return s;
+  const int64_t nepochs = (nsteps + tsteps - 1) / tsteps;
+  if (nepochs & 1) {
+    *newest = f2;
+    *previous = f1;
+  }
   return PS_OK;
 }
 

@@ -36,7 +36,8 @@ class Simulation:
     (default: the scheme radius); periodic grids hold n^2 independent nodes."""
 
     def __init__(self, scheme, n: int, lam: float, bc: str = "dirichlet", ring: int | None = None,
-                 dtype: str = "f64", arith: str = "ref", c: float = 1.0, tsteps: int = 1):
+                 dtype: str = "f64", arith: str = "ref", c: float = 1.0, tsteps: int = 1,
+                 tile: int = 0):
         self.spec: SchemeSpec = named_scheme(scheme) if isinstance(scheme, str) else scheme
         if bc not in nat.BC:
             raise ValueError(f"bc must be one of {tuple(nat.BC)}, got {bc!r}")
@@ -50,11 +51,17 @@ class Simulation:
         if tsteps not in (1, 2, 3, 4, 5, 6):
             raise ValueError(f"tsteps must be 1..6, got {tsteps}")
         self.tsteps = int(tsteps)
+        # tile > 0: march() runs small Dirichlet f64 grids tile-resident (ps_march_tile: one
+        # cooperative launch, `tile` updates per shared-memory pass) when the grid qualifies
+        if not 0 <= int(tile) <= 16:
+            raise ValueError(f"tile must be 0..16, got {tile}")
+        self.tile = int(tile)
+        self._tile_ok = None
         # periodic blocked passes read wrap-around images R*T deep
         ghost = max(2, radius * tsteps) if bc == "periodic" else max(2, radius)
         self.grid = nat.make_grid(self.rows, self.rows, ghost, self.ring, bc, dtype, arith)
         # temporal blocking writes two new levels while both inputs are still read: 4 levels
-        self.levels = [nat.Level(self.grid) for _ in range(3 if tsteps == 1 else 4)]
+        self.levels = [nat.Level(self.grid) for _ in range(3 if tsteps == 1 and not tile else 4)]
         self.previous = None
         self.t_first_u = nat.make_table(evaluate_table(self.spec.first_u, self.lam))
         self.t_first_v = nat.make_table(evaluate_table(self.spec.first_v, self.lam))
@@ -127,7 +134,13 @@ class Simulation:
         """``nsteps`` two-step updates, rotating the three levels in place."""
         if self.newest is None:
             raise RuntimeError("call first_step() before march()")
-        if self.tsteps == 1:
+        if self.tile and self._tile_ok is None:
+            self._tile_ok = nat.tile_supported(self.grid, self.t_two, self.tile)
+        if self.tile and self._tile_ok:
+            self.newest, self.previous = nat.march_tile(self.grid, self.levels[:4], nsteps,
+                                                        self.t_two, self.tile, self.newest,
+                                                        self.previous, stream)
+        elif self.tsteps == 1 and not self.tile:
             self.newest = nat.march(self.grid, self.levels, nsteps, self.t_two, self.newest, stream)
             self.previous = (self.newest + 2) % 3
         else:
