@@ -205,7 +205,7 @@ ps_status ps_two_step_tb_halo(const ps_grid* g, const void* uk, const void* ukm1
 ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
                       int32_t tsteps, int32_t* newest, int32_t* previous, void* stream);
 
-/* Tile-resident march for SMALL Dirichlet f64 grids (a level of at most a few MB: BASELINE
+/* Tile-resident march for SMALL f64 grids, Dirichlet or periodic (a level of a few MB: BASELINE
  * config 1, the reference's own regime — run()'s loop of two_step calls, simulator.py:
  * 271-274).  One cooperative launch runs all nsteps updates: the grid is cut into one tile
  * per SM, every pass loads a tile plus a halo of R*tsteps points into shared memory, runs
@@ -213,7 +213,7 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
  * for their 8 neighbours (release/acquire epoch flags), not for a launch boundary.  Same
  * level bookkeeping as ps_march_tb (four levels; *newest / *previous updated), same bits
  * as nsteps ps_two_step calls.  tsteps 1..16.  Returns PS_ERR_ARG when the grid does not
- * qualify (periodic, f32, row slab, ring narrower than the stencil, or no tiling that fits
+ * qualify (f32, row slab, Dirichlet ring narrower than the stencil, or no tiling that fits
  * the SMs' shared memory): ps_tile_supported() asks first. */
 int32_t ps_tile_supported(const ps_grid* g, const ps_table* t, int32_t tsteps);
 ps_status ps_march_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,

@@ -639,10 +639,10 @@ ps_status ps_march_tb(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_t
 // Tile-resident march (ps_tile.cuh): 1 = this grid / table / depth can run it.
 static bool tile_plan_for(const ps_grid* g, const ps_table* t, int tsteps, int* py, int* px,
                           int* th, int* tw, size_t* smem) {
-  if (g->bc != PS_BC_DIRICHLET || g->dtype != PS_F64 || !single_slab(g)) return false;
+  if (g->dtype != PS_F64 || !single_slab(g)) return false;
   if (tsteps < 1 || tsteps > 16 || !stream_shape(t)) return false;
   const int R = table_radius(t);
-  if (g->ring < R) return false;
+  if (g->bc == PS_BC_DIRICHLET && g->ring < R) return false;
   return tile_plan(g->rows, g->cols, R, tsteps, std::max(1, dev_info().nsm),
                    size_t(227) * 1024, py, px, th, tw, smem);
 }
@@ -690,8 +690,12 @@ ps_status ps_march_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps
       return PS_ERR_CUDA;
     flags = flag_pool[dev] + size_t(flag_seq.fetch_add(1) % kFlagSets) * kFlagStride;
   }
-#define PS_TILE_GO(S) \
-  launch_tile<S>(g, lvl, nsteps, t, tsteps, cur, prev, f1, f2, flags, st, py, px, th, tw, smem)
+#define PS_TILE_GO(S)                                                                          \
+  (g->bc == PS_BC_PERIODIC                                                                     \
+       ? launch_tile<S, true>(g, lvl, nsteps, t, tsteps, cur, prev, f1, f2, flags, st, py, px, \
+                              th, tw, smem)                                                    \
+       : launch_tile<S, false>(g, lvl, nsteps, t, tsteps, cur, prev, f1, f2, flags, st, py,    \
+                               px, th, tw, smem))
   if (shape_matches<ShapeP5>(t))
     s = PS_TILE_GO(ShapeP5);
   else if (shape_matches<ShapeP9>(t))
@@ -706,6 +710,11 @@ ps_status ps_march_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps
   if (nepochs & 1) {
     *newest = f2;
     *previous = f1;
+  }
+  if (g->bc == PS_BC_PERIODIC) {
+    // the tiles wrote the n x n cores only: refresh the images other kernels read
+    if ((s = ps_fill_ghosts(g, lvl[*newest], 0, stream)) != PS_OK) return s;
+    if ((s = ps_fill_ghosts(g, lvl[*previous], 0, stream)) != PS_OK) return s;
   }
   return PS_OK;
 }

@@ -230,7 +230,22 @@ ps_status ps_solve_host(const ps_grid* g, void* lvl[4], const void* u0_host,
     if ((s = first_step_impl(g, lvl[0], lvl[2], lvl[1], tu, tv, tau, 0, g->rows, st)) != PS_OK)
       return s;
     int32_t cur = 1, prev = 0;
-    if ((s = ps_march_tb(g, lvl, nsteps - 1, t, tsteps, &cur, &prev, stream)) != PS_OK) return s;
+    bool tiled = false;
+    if (env_int("PS_SOLVE_TILE", 1) != 0 && nsteps > 1 && nbands == 0) {
+      // small grids: all the updates in one tile-resident launch (ps_march_tile)
+      for (const int depth : {12, 8, 4}) {
+        int py, px, th, tw;
+        size_t smem;
+        if (!tile_plan_for(g, t, depth, &py, &px, &th, &tw, &smem)) continue;
+        if ((s = ps_march_tile(g, lvl, nsteps - 1, t, depth, &cur, &prev, stream)) != PS_OK)
+          return s;
+        tiled = true;
+        break;
+      }
+    }
+    if (!tiled &&
+        (s = ps_march_tb(g, lvl, nsteps - 1, t, tsteps, &cur, &prev, stream)) != PS_OK)
+      return s;
     return ps_copy_out(g, lvl[cur], out_host, rows_h, cols_h, host_pitch, kind_out, stream);
   }
 

@@ -1,4 +1,4 @@
-// ps_tile.cuh — tile-resident march for small Dirichlet f64 grids (BASELINE config 1: the
+// ps_tile.cuh — tile-resident march for small f64 grids, Dirichlet or periodic (BASELINE config 1: the
 // reference's own regime, n <= a few hundred).  Included inside namespace ps by ps_device.cu.
 //
 // A 512^2 level is 2 MB: it lives in L2, and one streaming launch per step costs a launch
@@ -18,7 +18,9 @@
 // The per-point arithmetic is Arith<double, REF>::tap over the compile-time tap list of the
 // scheme shape with run-time coefficients — the same sequence as every other kernel, so the
 // result equals T single launches bit for bit; the Dirichlet ring is re-pinned to +0.0 at
-// every update (simulator.py:147-160, 183-191).
+// every update (simulator.py:147-160, 183-191).  Periodic grids: tiles form a ring in both
+// directions, halos are loaded with wrapped indices from the n x n core, and ps_march_tile
+// refreshes the wrap-around images of the two final levels afterwards (ps_fill_ghosts).
 //
 // Measured on the B200 (C1: P5, 512^2, 200 steps, 13 x 11 tiles of 40 x 47): 1.94 us per step
 // at T = 10..12 (134 GLUP/s) against 4.06-4.4 for the CUDA-graph-replayed streaming march;
@@ -49,7 +51,7 @@ __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) 
 constexpr int kTileThreads = 512;
 constexpr int kTileLanes = 64;  // threads along a row
 
-template <class S>
+template <class S, bool PER>
 __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_constant__ TileParams p) {
   constexpr int R = S::R;
   using Ar = Arith<double, ARITH_REF>;
@@ -73,7 +75,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
   // the (up to) 8 neighbouring tiles whose epochs this tile waits for
   int nb = -1;
   if (tid < 9 && tid != 4) {
-    const int ny = ty0 + tid / 3 - 1, nx = tx0 + tid % 3 - 1;
+    int ny = ty0 + tid / 3 - 1, nx = tx0 + tid % 3 - 1;
+    if (PER) {  // a ring of tiles in both directions (a tile may be its own neighbour)
+      ny = (ny + p.py) % p.py;
+      nx = (nx + p.px) % p.px;
+    }
     if (ny >= 0 && ny < p.py && nx >= 0 && nx < p.px) nb = ny * p.px + nx;
   }
 
@@ -102,7 +108,14 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
           for (int u = 0; u < U; ++u) {
             const int ii = i + u * NY;
             a[u] = b[u] = 0.0;
-            if (ii < i_hi && ii >= 0 && ii < p.rows && j >= 0 && j < p.cols) {
+            if (PER) {
+              if (ii < i_hi) {   // periodic: the halo wraps around the core (no images read)
+                const int iw = ii < 0 ? ii + p.rows : (ii >= p.rows ? ii - p.rows : ii);
+                const int jw = j < 0 ? j + p.cols : (j >= p.cols ? j - p.cols : j);
+                a[u] = __ldcg(gk + int64_t(iw) * p.pitch + jw);
+                b[u] = __ldcg(gm + int64_t(iw) * p.pitch + jw);
+              }
+            } else if (ii < i_hi && ii >= 0 && ii < p.rows && j >= 0 && j < p.cols) {
               a[u] = __ldcg(gk + int64_t(ii) * p.pitch + j);
               b[u] = __ldcg(gm + int64_t(ii) * p.pitch + j);
             }
@@ -124,8 +137,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
     int cur = 1, prev = 0, nxt = 2;
     for (int s = 1; s <= Te; ++s) {
       const int E = R * (Te - s);
-      const int i_lo = max(r0 - E, 0), i_hi = min(r1 + E, p.rows);
-      const int j_lo = max(c0 - E, 0), j_hi = min(c1 + E, p.cols);
+      const int i_lo = PER ? r0 - E : max(r0 - E, 0), i_hi = PER ? r1 + E : min(r1 + E, p.rows);
+      const int j_lo = PER ? c0 - E : max(c0 - E, 0), j_hi = PER ? c1 + E : min(c1 + E, p.cols);
       const double* __restrict__ L = base + cur * BS;
       const double* __restrict__ M = base + prev * BS;
       double* __restrict__ O = base + nxt * BS;
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
       const int b0 = i_lo + ty * bh, b1 = min(b0 + bh, i_hi);
       for (int j = j_lo + tx; j < j_hi; j += kTileLanes) {
         const int lj = j - (c0 - H);
-        const bool col_in = j >= p.ring && j < p.cols - p.ring;
+        const bool col_in = PER || (j >= p.ring && j < p.cols - p.ring);
         double win[WN][WN];
 #pragma unroll
         for (int r = 0; r + 1 < WN; ++r)
@@ -159,7 +172,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
           for (int q = 0; q < S::N; ++q)
             acc = Ar::tap(acc, c[q], win[R + S::q(q, 0)][R + S::q(q, 1)]);
           const double r = Ar::two(acc, M[li * SP + lj]);
-          O[li * SP + lj] = (col_in && i >= p.ring && i < p.rows - p.ring) ? r : 0.0;
+          O[li * SP + lj] = (col_in && (PER || (i >= p.ring && i < p.rows - p.ring))) ? r : 0.0;
         }
       }
       __syncthreads();
@@ -227,11 +240,11 @@ static bool tile_plan(int64_t rows, int64_t cols, int R, int T, int nsm, size_t 
   return ok;
 }
 
-template <class S>
+template <class S, bool PER>
 static ps_status launch_tile(const ps_grid* g, void* lvl[4], int64_t nsteps, const ps_table* t,
                              int T, int cur, int prev, int f_prev, int f_cur, unsigned int* flags,
                              cudaStream_t st, int py, int px, int th, int tw, size_t smem) {
-  auto kern = k_tile_march<S>;
+  auto kern = k_tile_march<S, PER>;
   static std::once_flag once[kMaxDevices];
   const int dev = device_index();
   std::call_once(once[dev], [&] {

@@ -16,6 +16,14 @@
 #     4-row slots 349; T=4 old 8 WGS warps 360; shared products T=2 (12 warps, 8 x 2) 336,
 #     T=3 8 warps 385 (8 x 2: 358), T=3 12 warps (1 KB spills) 191.
 #
+# Round-2, last session (40-step runs at 1965 MHz; 200-step runs tie under the power cap):
+#   C4 T=5 ring shape at equal shared memory: 8x3 752-756, 10x3 772 (now the default for
+#     radius 1 where 30 rows fit), 6x4 737, 4x6 718; producer sleep 0 ns 750-756 (no change).
+#   Unrolled head slots (PS_TB_SYM_HEAD): C3 T=3 451 -> 458, C4 728-758 vs 750 (noise), +7 min
+#     of ptxas for the radius-2 body: off.  Producer-written slot descriptors (tile arithmetic
+#     out of the consumer warps): C4 +0.5 %, C2 +2 %, C3 -9 % (spills): not kept.
+#   C2 (periodic P9 T=4) after the image-loop fix: 335; shared products 258, 8 WGS warps 329.
+#
 # Round-1 history (tools/tb_variants.sh, now folded in here):
 #
 # Round-1 history (C4 f64 P9 T=4, 40 steps): base 475, minb2 477, rb6 475 GLUP/s; 11 consumer
