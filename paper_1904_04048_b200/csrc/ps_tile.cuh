@@ -159,20 +159,24 @@ __global__ void __launch_bounds__(kTileThreads, 1) k_tile_march(const __grid_con
 #pragma unroll
           for (int x = 0; x < WN; ++x)
             win[r + 1][x] = (b0 < b1) ? L[(b0 - (r0 - H) - R + r) * SP + lj - R + x] : 0.0;
-        for (int i = b0; i < b1; ++i) {
-          const int li = i - (r0 - H);
+        // WN rows per trip with the window rotating through compile-time slots (logical row
+        // r of trip step u lives in slot (r + 1 + u) % WN), so no register moves
+        for (int ib = b0; ib < b1; ib += WN) {
 #pragma unroll
-          for (int r = 0; r + 1 < WN; ++r)
+          for (int u = 0; u < WN; ++u) {
+            const int i = ib + u;
+            if (i < b1) {
+              const int li = i - (r0 - H);
 #pragma unroll
-            for (int x = 0; x < WN; ++x) win[r][x] = win[r + 1][x];
+              for (int x = 0; x < WN; ++x) win[u % WN][x] = L[(li + R) * SP + lj - R + x];
+              double acc = Ar::zero();
 #pragma unroll
-          for (int x = 0; x < WN; ++x) win[WN - 1][x] = L[(li + R) * SP + lj - R + x];
-          double acc = Ar::zero();
-#pragma unroll
-          for (int q = 0; q < S::N; ++q)
-            acc = Ar::tap(acc, c[q], win[R + S::q(q, 0)][R + S::q(q, 1)]);
-          const double r = Ar::two(acc, M[li * SP + lj]);
-          O[li * SP + lj] = (col_in && (PER || (i >= p.ring && i < p.rows - p.ring))) ? r : 0.0;
+              for (int q = 0; q < S::N; ++q)
+                acc = Ar::tap(acc, c[q], win[(R + S::q(q, 0) + 1 + u) % WN][R + S::q(q, 1)]);
+              const double r = Ar::two(acc, M[li * SP + lj]);
+              O[li * SP + lj] = (col_in && (PER || (i >= p.ring && i < p.rows - p.ring))) ? r : 0.0;
+            }
+          }
         }
       }
       __syncthreads();
