@@ -352,6 +352,34 @@ def cpu_baseline(args, cfg):
     return out
 
 
+def single_config(cfg, T, tile_depth):
+    """`config` of the single-GPU arm; `--impl reference` prints the same object (it runs on
+    this arm's config; its own threading is in `cpu_baseline`)."""
+    width = cfg["n"] + 1 if cfg["bc"] == "dirichlet" else cfg["n"]
+    level = width * width * (8 if cfg["dtype"] == "f64" else 4)
+    return {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
+            "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
+            "parallelism": "single GPU", "temporal_blocking": T,
+            "tile_resident_depth": tile_depth,
+            "l2": f"inputs larger than L2: {level / 1e9:.2f} GB per level, "
+                  "streamed from HBM every launch" if level > 126e6 else
+                  "grid fits in L2 (latency-bound correctness config)"}
+
+
+def dist_config(cfg, T, world, halo_rows, transport, graphed):
+    """`config` of the row-slab arm (one rank per GPU); shared with `--impl reference`."""
+    return {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
+            "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
+            "temporal_blocking": T,
+            "parallelism": f"row slabs x{world}, {halo_rows}-row halo "
+                           + ("over NCCL send/recv" if transport == "nccl" else
+                              "stored into peer ghost rows by the fused kernel "
+                              "(CUDA IPC over NVLink)")
+                           + ", overlapped with the interior update",
+            "cuda_graph": graphed,
+            "l2": "inputs larger than L2"}
+
+
 def reference_arm(args, cfg, cfg_name):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -387,14 +415,23 @@ def reference_arm(args, cfg, cfg_name):
     value = lup / dt / 1e9
     sample = (f"{srows} full-width rows x {width} cols per step (of {cfg['n'] + 1} rows), "
               f"{args.steps} steps")
+    # the config object of the GPU arm launched with the same flags
+    T = args.tsteps if args.tsteps > 0 else cfg.get("tb", 1)
+    if world > 1 or args.force_dist:
+        from paper_1904_04048_b200.scheme import named_scheme as _ns
+        arm_cfg = dist_config(cfg, T, world, _ns(cfg["scheme"]).radius * T, args.transport,
+                              not args.no_graph)
+    else:
+        tile = args.tile if args.tile >= 0 else (cfg.get("tile", 0) if T == 1 else 0)
+        arm_cfg = single_config(cfg, T, tile)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GLUP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
-        "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
-                   "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
-                   "parallelism": "cpu (OpenMP over rows)"},
+        "config": arm_cfg,
+        "config_note": "the GPU arm's config (the workload both arms run); this arm itself is "
+                       "the reference arithmetic on the host cores, see cpu_baseline",
         "cpu_baseline": {"value": value, "unit": "GLUP/s", "cores": threads, "kind": "port",
                          "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
                          "sample": sample + "; oracle/ps_oracle.c (reference arithmetic, "
@@ -571,13 +608,7 @@ def gpu_arm_single(args, cfg, cfg_name):
         "warmup": m["warmup"], "ms_per_step": m["total_ms"] / m["K"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
         "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
-        "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
-                   "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
-                   "parallelism": "single GPU", "temporal_blocking": T,
-                   "tile_resident_depth": tile if m["tiled"] else 0,
-                   "l2": f"inputs larger than L2: {sim.level_bytes / 1e9:.2f} GB per level, "
-                         "streamed from HBM every launch" if sim.level_bytes > 126e6 else
-                         "grid fits in L2 (latency-bound correctness config)"},
+        "config": single_config(cfg, T, tile if m["tiled"] else 0),
         "timing": {"regions_ms": m["regions_ms"], "reported": "median region",
                    "what": f"{len(m['regions_ms'])} back-to-back regions of exactly "
                            f"{m['K']} steps, each between CUDA events on the launching stream"},
@@ -796,16 +827,7 @@ def gpu_arm_dist(args, cfg, cfg_name):
             "warmup": m["warmup"], "ms_per_step": total_ms / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg["dtype"],
             "data": "synthetic (seeded initial data per SURVEY.md §8d D1, generated on the device)",
-            "config": {"workload": cfg["desc"], "scheme": cfg["scheme"], "nodes": cfg["n"] + 1,
-                       "lambda": cfg["lam"], "bc": cfg["bc"], "arith": cfg["arith"],
-                       "temporal_blocking": T,
-                       "parallelism": f"row slabs x{world}, {slab.R * T}-row halo "
-                                      + ("over NCCL send/recv" if args.transport == "nccl" else
-                                         "stored into peer ghost rows by the fused kernel "
-                                         "(CUDA IPC over NVLink)")
-                                      + ", overlapped with the interior update",
-                       "cuda_graph": m["graphed"],
-                       "l2": "inputs larger than L2"},
+            "config": dist_config(cfg, T, world, slab.R * T, args.transport, m["graphed"]),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(cfg_name, T),
                          "peak_source": peak_src + " (per GPU; whole-step time incl. exchange)",

@@ -296,3 +296,28 @@ def test_csv_writer_matches_numpy_savetxt(tmp_path):
         assert p1.read_bytes() == p2.read_bytes()
     loaded = np.loadtxt(p2, delimiter=",")
     assert loaded.shape == (7, 9)
+
+
+def test_bench_reference_arm_prints_the_gpu_arms_config():
+    """`bench.py --impl reference` runs without a GPU and reports the GPU arm's own `config`
+    object (same workload, same keys), its own threading under `cpu_baseline`."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    sys.path.insert(0, root)
+    try:
+        import bench
+    finally:
+        sys.path.pop(0)
+    cfg = bench.CONFIGS["C1"]
+    assert line["config"] == bench.single_config(cfg, 1, cfg.get("tile", 0))
+    assert line["impl"] == "reference" and line["gpu_launches"] == 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
