@@ -602,7 +602,9 @@ def gpu_arm_single(args, cfg, cfg_name):
                 f"region's updates, {tile} per shared-memory pass; levels stay in L2 / shared "
                 "memory, so the 3-words-per-update figure is algorithmic, not DRAM traffic")
         roof["note"] = note
-        dram = {"note": "L2-resident grid: no DRAM-side model (see roofline.note)"}
+        roof["traffic"] = load_traffic(cfg_name + "_tile")
+        dram = {"note": "L2-resident grid: no DRAM-side model (see roofline.note)",
+                "ncu_bytes_per_launch": roof["traffic"]}
     line = {
         "metric": METRIC, "value": m["value"], "unit": "GLUP/s", "n_gpus": 1, "steps": m["K"],
         "warmup": m["warmup"], "ms_per_step": m["total_ms"] / m["K"], "higher_is_better": True,
