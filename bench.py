@@ -972,6 +972,15 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     if world > 1 or args.force_dist:
+        if "WORLD_SIZE" not in os.environ:
+            # --force-dist without torchrun: a world of one on the loopback rendezvous
+            import socket
+            with socket.socket() as sock:
+                sock.bind(("127.0.0.1", 0))
+                port = sock.getsockname()[1]
+            for k, v in (("RANK", "0"), ("LOCAL_RANK", "0"), ("WORLD_SIZE", "1"),
+                         ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", str(port))):
+                os.environ.setdefault(k, v)
         gpu_arm_dist(args, cfg, args.config)
     else:
         gpu_arm_single(args, cfg, args.config)
